@@ -1,0 +1,156 @@
+/*
+ * qsb.h — C ABI of the B200 QAOA statevector backend ("qsb").
+ *
+ * This is the drop-in boundary for the reference's kernel-set plugin seam:
+ * `qaoasim.kernels.get(name)` returns a module exposing 14 data-parallel
+ * functions over 2^n arrays (/root/reference/pkg/src/qaoasim/kernels/__init__.py:47-61,
+ * numba_impl.py:247-260).  Every such function has a `qsb_*` counterpart here
+ * operating on DEVICE pointers, plus the allocation hooks that backend.py
+ * performs with np.empty today (backend.py:133,150,165,264,268) and the fused
+ * entry points the fast path uses (simulate / value_and_grad / sample).
+ *
+ * Conventions
+ *   - amplitudes are complex128 interleaved (re, im) = double[2*len]; tables are f64.
+ *   - every function returns an int status (QSB_OK == 0); on failure a
+ *     thread-local message is available from qsb_last_error().  The Python
+ *     wrapper maps QSB_ENOMEM -> ResourceError, QSB_EINVAL -> ContractViolation,
+ *     anything else -> RuntimeError (errors.py:4-19 of the reference).
+ *   - all launches go on the context's own CUDA stream; functions that return
+ *     a scalar synchronise that stream only.  Distinct contexts may be used
+ *     from distinct host threads concurrently.
+ *   - no torch types, no C++ types: plain pointers and sizes.
+ */
+#ifndef QSB_H
+#define QSB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QSB_OK 0
+#define QSB_EINVAL 1
+#define QSB_ENOMEM 2
+#define QSB_ECUDA 3
+#define QSB_ENODEV 4
+
+/* flags for the fused entry points */
+#define QSB_EXACT 1u      /* FMA-free arithmetic + ascending qubit order: bit-identical
+                             to the numba kernel set (numba_impl.py:47-72) */
+#define QSB_FROM_PLUS 2u  /* (simulate) start from |+>, the input state is not read */
+
+typedef struct qsb_ctx qsb_ctx;
+typedef struct qsb_table qsb_table;
+
+/* ---------------------------------------------------------------- errors */
+const char* qsb_last_error(void);
+int qsb_abi_version(void);
+
+/* ------------------------------------------------------ device / context */
+int qsb_device_count(int* out);
+/* one context = one device + one CUDA stream + scratch (backend.py:35 BackendContext) */
+int qsb_ctx_create(int device, qsb_ctx** out);
+int qsb_ctx_destroy(qsb_ctx* ctx);
+int qsb_ctx_sync(qsb_ctx* ctx);
+int qsb_ctx_device(qsb_ctx* ctx, int* device);
+/* SM count and free/total device memory, for sizing */
+int qsb_ctx_info(qsb_ctx* ctx, int* num_sms, uint64_t* free_bytes, uint64_t* total_bytes);
+/* device-side timing on the context stream (CUDA events) */
+int qsb_timer_start(qsb_ctx* ctx);
+int qsb_timer_stop(qsb_ctx* ctx, double* ms);
+/* live per-kernel profile: CUDA events around every fused sweep launched between
+ * begin and end.  out[3k..3k+2] = {launches, total ms, algorithmic bytes} for
+ * kind k (0: single-vector sweep, 1: bra/ket sweep). */
+int qsb_prof_begin(qsb_ctx* ctx);
+int qsb_prof_end(qsb_ctx* ctx, double* out, int nkinds);
+/* host<->device bytes the library has copied on this context (monotone) */
+int qsb_ctx_xfer(qsb_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
+/* number of qsb kernel launches issued on this context (monotone) */
+int qsb_ctx_launches(qsb_ctx* ctx, uint64_t* out);
+
+/* ----------------------------------------------------- memory (backend.py allocation hooks) */
+int qsb_alloc(qsb_ctx* ctx, uint64_t bytes, void** dptr);            /* np.empty, backend.py:133,165 */
+int qsb_free(qsb_ctx* ctx, void* dptr);                              /* eager release (StateBuffer.free) */
+int qsb_h2d(qsb_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+int qsb_d2h(qsb_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+int qsb_d2d(qsb_ctx* ctx, void* dst, const void* src, uint64_t bytes); /* clone_state, backend.py:149 */
+int qsb_h2d_async(qsb_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+int qsb_d2h_async(qsb_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+int qsb_host_alloc(uint64_t bytes, void** hptr);                     /* pinned host memory */
+int qsb_host_free(void* hptr);
+
+/* ------------------------------------------------------- the 14-function kernel set
+ * Each mirrors qaoasim/kernels/numba_impl.py (file:line in the comment) with the
+ * same arithmetic (FMA-free, same association), so results are bit-identical to
+ * the "accelerated" set on identical inputs (phase factors: see qsb_phase_by_table). */
+int qsb_fill_plus(qsb_ctx* ctx, double* amps, uint64_t len);                          /* :40-44 */
+/* amps *= cos(-gamma*t)+i sin(-gamma*t).  Integer-valued tables with a small range
+ * use a host-libm LUT (bit-identical to numba); otherwise device sincos. :47-51 */
+int qsb_phase_by_table(qsb_ctx* ctx, double* amps, const double* table, uint64_t len, double gamma);
+int qsb_diag_scale(qsb_ctx* ctx, double* amps, const double* table, uint64_t len);    /* :54-57 */
+int qsb_rx_qubit(qsb_ctx* ctx, double* amps, uint64_t len, int j, double c, double s); /* :60-72 */
+int qsb_weighted_probs(qsb_ctx* ctx, const double* amps, const double* table, double* out, uint64_t len); /* :75-79 */
+int qsb_probs(qsb_ctx* ctx, const double* amps, double* out, uint64_t len);           /* :82-86 */
+/* neighbour-pair tree with zero padding, bit-identical to tree_sum :114-126 */
+int qsb_tree_sum(qsb_ctx* ctx, const double* vals, uint64_t len, double* out);
+int qsb_reduce_min(qsb_ctx* ctx, const double* vals, uint64_t len, double* out);      /* :129-136 */
+int qsb_reduce_max(qsb_ctx* ctx, const double* vals, uint64_t len, double* out);      /* :138-144 */
+int qsb_inner(qsb_ctx* ctx, const double* a, const double* b, uint64_t len, double out[2]);          /* :147-170 */
+int qsb_diag_inner(qsb_ctx* ctx, const double* a, const double* table, const double* b, uint64_t len, double out[2]); /* :173-197 */
+int qsb_xsum(qsb_ctx* ctx, const double* a, const double* b, uint64_t len, int n_qubits, double out[2]); /* :200-226 */
+int qsb_precompute_table(qsb_ctx* ctx, const double* weights, const int64_t* masks, uint64_t num_terms,
+                         double* out, uint64_t len);                                   /* :229-238 (host w/m) */
+int qsb_pairwise_level(qsb_ctx* ctx, const double* src, double* dst, uint64_t dst_len); /* :241-244 */
+
+/* ------------------------------------------------------- cost table object
+ * costpoly.precompute (costpoly.py:126-133): fill the 2^n table on device, record
+ * min/max, and — when every value is an integer and max-min < 65536 — a compact
+ * uint8/uint16 index table (value = min + idx) used by the fused sweeps for
+ * 1-2 B/amp table traffic and exact host-libm phase LUTs. `values` is caller
+ * owned (the RealBuffer of CostTable.values). */
+int qsb_table_create(qsb_ctx* ctx, int n, const double* weights, const int64_t* masks, uint64_t num_terms,
+                     double* values, double* min_out, double* max_out, qsb_table** out);
+/* wrap an already-filled device table (e.g. uploaded by the user) */
+int qsb_table_wrap(qsb_ctx* ctx, int n, double* values, double* min_out, double* max_out, qsb_table** out);
+int qsb_table_destroy(qsb_table* t);
+/* 0: fp64 + device sincos, 1: uint8 index, 2: uint16 index */
+int qsb_table_kind(qsb_table* t, int* kind, int* num_values);
+/* phase_by_table through a table object: exact host-libm LUT when compact */
+int qsb_table_phase(qsb_ctx* ctx, qsb_table* t, double* amps, double gamma);
+/* host-only: the LUT entries (cos, sin)(-gamma * (vmin + k)) the library builds */
+int qsb_phase_lut_host(double gamma, double vmin, int nvals, double* out);
+
+/* ------------------------------------------------------- fused hot path
+ * Layer = phase exp(-i gamma C) then Rx(-2 beta) on every qubit (circuit.py:98-103).
+ * The phase is fused into the first mixer sweep; ~12 qubits are applied per HBM
+ * sweep (shared-memory exchange between register-resident butterfly phases). */
+int qsb_simulate(qsb_ctx* ctx, qsb_table* t, double* amps, int p, const double* gammas,
+                 const double* betas, unsigned flags);
+/* simulate + <psi|C|psi> taken from the last sweep (circuit.expectation, circuit.py:116-118) */
+int qsb_simulate_expect(qsb_ctx* ctx, qsb_table* t, double* amps, int p, const double* gammas,
+                        const double* betas, unsigned flags, double* expect_out);
+/* Rx(theta) on every qubit of amps (backend.apply_rx_layer, backend.py:200-207) */
+int qsb_rx_layer(qsb_ctx* ctx, double* amps, int n, double theta, unsigned flags);
+/* <psi|C|psi> (circuit.expectation_of_state, circuit.py:106-113, without the clamp) */
+int qsb_expectation(qsb_ctx* ctx, qsb_table* t, const double* amps, unsigned flags, double* out);
+/* expectation + adjoint gradient (adjoint.py:37-77): one forward, one backward walk
+ * over exactly two statevectors (ket = amps, bra = caller-provided scratch).
+ * If `skip_forward` != 0 the caller guarantees amps already holds simulate(params).
+ * value may be NULL.  d_gammas/d_betas: host arrays of length p. */
+int qsb_value_and_grad(qsb_ctx* ctx, qsb_table* t, double* ket, double* bra, int p,
+                       const double* gammas, const double* betas, unsigned flags, int skip_forward,
+                       double* value, double* d_gammas, double* d_betas);
+/* sampling (backend.sample_indices, backend.py:261-299 + sampling.draw): probability
+ * tree with the reference's pairwise association, splitmix64 uniforms (rng.py:30-37),
+ * root-to-leaf descent; costs gathered from the table on device.
+ * t may be NULL (indices only; cost_out ignored).
+ * Writes total (tree root) before checking normalisation; returns QSB_EINVAL with
+ * "not normalized" when |root-1| > 1e-9.  idx/cost are HOST arrays of `shots`. */
+int qsb_sample(qsb_ctx* ctx, qsb_table* t, const double* amps, int n, uint64_t shots, uint64_t seed,
+               int64_t* idx_out, double* cost_out, double* total_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QSB_H */

@@ -1,0 +1,309 @@
+"""ctypes binding of libqsb.so (include/qsb.h) and the device-array type.
+
+This is the only place Python touches the C ABI.  Status codes map onto the
+reference's error convention (errors.py:4-19): QSB_ENOMEM -> ResourceError,
+QSB_EINVAL -> ContractViolation, everything else -> RuntimeError.  There is no
+CPU fallback: if the library or a B200 is missing, every device operation
+raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+import numpy as np
+
+from .errors import ContractViolation, ResourceError
+
+_LIB_PATH = Path(__file__).resolve().parent / "libqsb.so"
+
+QSB_OK, QSB_EINVAL, QSB_ENOMEM, QSB_ECUDA, QSB_ENODEV = 0, 1, 2, 3, 4
+QSB_EXACT = 1
+QSB_FROM_PLUS = 2
+
+_vp = C.c_void_p
+_u64 = C.c_uint64
+_i32 = C.c_int
+_dbl = C.c_double
+_dp = C.POINTER(C.c_double)
+
+# name -> argtypes (all return int status unless listed in _RESTYPES)
+_SIGS = {
+    "qsb_last_error": [],
+    "qsb_abi_version": [],
+    "qsb_device_count": [C.POINTER(_i32)],
+    "qsb_ctx_create": [_i32, C.POINTER(_vp)],
+    "qsb_ctx_destroy": [_vp],
+    "qsb_ctx_sync": [_vp],
+    "qsb_ctx_device": [_vp, C.POINTER(_i32)],
+    "qsb_ctx_info": [_vp, C.POINTER(_i32), C.POINTER(_u64), C.POINTER(_u64)],
+    "qsb_timer_start": [_vp],
+    "qsb_timer_stop": [_vp, _dp],
+    "qsb_ctx_launches": [_vp, C.POINTER(_u64)],
+    "qsb_ctx_xfer": [_vp, C.POINTER(_u64), C.POINTER(_u64)],
+    "qsb_prof_begin": [_vp],
+    "qsb_prof_end": [_vp, _dp, _i32],
+    "qsb_alloc": [_vp, _u64, C.POINTER(_vp)],
+    "qsb_free": [_vp, _vp],
+    "qsb_h2d": [_vp, _vp, _vp, _u64],
+    "qsb_d2h": [_vp, _vp, _vp, _u64],
+    "qsb_d2d": [_vp, _vp, _vp, _u64],
+    "qsb_h2d_async": [_vp, _vp, _vp, _u64],
+    "qsb_d2h_async": [_vp, _vp, _vp, _u64],
+    "qsb_host_alloc": [_u64, C.POINTER(_vp)],
+    "qsb_host_free": [_vp],
+    "qsb_fill_plus": [_vp, _vp, _u64],
+    "qsb_phase_by_table": [_vp, _vp, _vp, _u64, _dbl],
+    "qsb_diag_scale": [_vp, _vp, _vp, _u64],
+    "qsb_rx_qubit": [_vp, _vp, _u64, _i32, _dbl, _dbl],
+    "qsb_weighted_probs": [_vp, _vp, _vp, _vp, _u64],
+    "qsb_probs": [_vp, _vp, _vp, _u64],
+    "qsb_tree_sum": [_vp, _vp, _u64, _dp],
+    "qsb_reduce_min": [_vp, _vp, _u64, _dp],
+    "qsb_reduce_max": [_vp, _vp, _u64, _dp],
+    "qsb_inner": [_vp, _vp, _vp, _u64, _dp],
+    "qsb_diag_inner": [_vp, _vp, _vp, _vp, _u64, _dp],
+    "qsb_xsum": [_vp, _vp, _vp, _u64, _i32, _dp],
+    "qsb_precompute_table": [_vp, _vp, _vp, _u64, _vp, _u64],
+    "qsb_pairwise_level": [_vp, _vp, _vp, _u64],
+    "qsb_table_create": [_vp, _i32, _vp, _vp, _u64, _vp, _dp, _dp, C.POINTER(_vp)],
+    "qsb_table_wrap": [_vp, _i32, _vp, _dp, _dp, C.POINTER(_vp)],
+    "qsb_table_destroy": [_vp],
+    "qsb_table_kind": [_vp, C.POINTER(_i32), C.POINTER(_i32)],
+    "qsb_table_phase": [_vp, _vp, _vp, _dbl],
+    "qsb_phase_lut_host": [_dbl, _dbl, _i32, _dp],
+    "qsb_simulate": [_vp, _vp, _vp, _i32, _dp, _dp, C.c_uint],
+    "qsb_simulate_expect": [_vp, _vp, _vp, _i32, _dp, _dp, C.c_uint, _dp],
+    "qsb_rx_layer": [_vp, _vp, _i32, _dbl, C.c_uint],
+    "qsb_expectation": [_vp, _vp, _vp, C.c_uint, _dp],
+    "qsb_value_and_grad": [_vp, _vp, _vp, _vp, _i32, _dp, _dp, C.c_uint, _i32, _dp, _dp, _dp],
+    "qsb_sample": [_vp, _vp, _vp, _i32, _u64, _u64, _vp, _vp, _dp],
+}
+_RESTYPES = {"qsb_last_error": C.c_char_p, "qsb_abi_version": _i32}
+
+# symbols declared in include/qsb.h (checked by the CPU test suite)
+HEADER_SYMBOLS = tuple(_SIGS)
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def library_path() -> Path:
+    return _LIB_PATH
+
+
+def load():
+    """Load libqsb.so (building it first if it is missing and nvcc exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not _LIB_PATH.exists():
+            from . import _build
+
+            _build.build()
+        lib = C.CDLL(str(_LIB_PATH))
+        for name, args in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = _RESTYPES.get(name, _i32)
+        _lib = lib
+        return lib
+
+
+def last_error() -> str:
+    return load().qsb_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == QSB_OK:
+        return
+    msg = last_error()
+    if what:
+        msg = f"{what}: {msg}"
+    if rc == QSB_EINVAL:
+        raise ContractViolation(msg)
+    if rc == QSB_ENOMEM:
+        raise ResourceError(msg)
+    raise RuntimeError(msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)
+
+
+def dptr(x) -> C.c_double:
+    return C.cast(x, _dp)
+
+
+def f64_ptr(arr: np.ndarray):
+    return arr.ctypes.data_as(_dp)
+
+
+# ---------------------------------------------------------------- device context
+class DeviceContext:
+    """One B200 + one CUDA stream (qsb_ctx).  Fails loudly without a GPU."""
+
+    def __init__(self, device: int = 0):
+        lib = load()
+        h = _vp()
+        check(lib.qsb_ctx_create(int(device), C.byref(h)), f"cannot open B200 device {device}")
+        self.handle = h
+        self.device = int(device)
+        self._closed = False
+
+    def sync(self) -> None:
+        call("qsb_ctx_sync", self.handle)
+
+    def info(self) -> tuple[int, int, int]:
+        sms, free, total = _i32(), _u64(), _u64()
+        call("qsb_ctx_info", self.handle, C.byref(sms), C.byref(free), C.byref(total))
+        return sms.value, free.value, total.value
+
+    def launches(self) -> int:
+        out = _u64()
+        call("qsb_ctx_launches", self.handle, C.byref(out))
+        return out.value
+
+    def xfer(self) -> tuple[int, int]:
+        """(host->device, device->host) bytes copied by the library so far."""
+        a, b = _u64(), _u64()
+        call("qsb_ctx_xfer", self.handle, C.byref(a), C.byref(b))
+        return a.value, b.value
+
+    def prof_begin(self) -> None:
+        call("qsb_prof_begin", self.handle)
+
+    def prof_end(self) -> dict:
+        """{kind: (launches, total_ms, algorithmic_bytes)} for kinds 'sweep1', 'sweep2'."""
+        out = (C.c_double * 6)()
+        call("qsb_prof_end", self.handle, out, 2)
+        return {"sweep1": (out[0], out[1], out[2]), "sweep2": (out[3], out[4], out[5])}
+
+    def timer_start(self) -> None:
+        call("qsb_timer_start", self.handle)
+
+    def timer_stop(self) -> float:
+        ms = _dbl()
+        call("qsb_timer_stop", self.handle, C.byref(ms))
+        return ms.value
+
+    def close(self) -> None:
+        if not self._closed and _lib is not None:
+            self._closed = True
+            _lib.qsb_ctx_destroy(self.handle)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DeviceArray:
+    """1-D array resident in B200 HBM.
+
+    Behaves like the host ndarray the reference stores in StateBuffer.data /
+    RealBuffer.data where the reference's tests touch it (backend.py:67-106):
+    `buf[:] = values` uploads, `np.asarray(buf)` / `buf.copy()` / iteration /
+    indexing download, `len()` and `==` work.  `free()` releases HBM eagerly.
+    """
+
+    __slots__ = ("dctx", "ptr", "dtype", "length", "table", "__weakref__")
+
+    def __init__(self, dctx: DeviceContext, length: int, dtype):
+        self.dctx = dctx
+        self.dtype = np.dtype(dtype)
+        self.length = int(length)
+        self.table = None  # attached qsb_table handle for cost tables
+        p = _vp()
+        check(load().qsb_alloc(dctx.handle, self.nbytes, C.byref(p)), "device allocation")
+        self.ptr = p.value
+
+    # -- ndarray-like surface
+    @property
+    def nbytes(self) -> int:
+        return self.length * self.dtype.itemsize
+
+    @property
+    def shape(self) -> tuple[int]:
+        return (self.length,)
+
+    @property
+    def size(self) -> int:
+        return self.length
+
+    @property
+    def ndim(self) -> int:
+        return 1
+
+    def __len__(self) -> int:
+        return self.length
+
+    def to_host(self, out: np.ndarray | None = None) -> np.ndarray:
+        if self.ptr is None:
+            raise ContractViolation("use of a freed device buffer")
+        if out is None:
+            out = np.empty(self.length, dtype=self.dtype)
+        call("qsb_d2h", self.dctx.handle, out.ctypes.data, self.ptr, self.nbytes)
+        return out
+
+    def from_host(self, values) -> None:
+        if self.ptr is None:
+            raise ContractViolation("use of a freed device buffer")
+        arr = np.ascontiguousarray(np.broadcast_to(np.asarray(values, dtype=self.dtype), (self.length,)))
+        call("qsb_h2d", self.dctx.handle, self.ptr, arr.ctypes.data, self.nbytes)
+
+    def __array__(self, dtype=None, copy=None):
+        host = self.to_host()
+        return host if dtype is None else host.astype(dtype)
+
+    def copy(self) -> np.ndarray:
+        return self.to_host()
+
+    def __iter__(self):
+        return iter(self.to_host())
+
+    def __getitem__(self, key):
+        return self.to_host()[key]
+
+    def __setitem__(self, key, value):
+        if isinstance(key, slice) and key == slice(None):
+            self.from_host(value)
+            return
+        host = self.to_host()
+        host[key] = value
+        self.from_host(host)
+
+    def __eq__(self, other):
+        if isinstance(other, (DeviceArray, np.ndarray, list, tuple, int, float, complex, np.generic)):
+            return self.to_host() == np.asarray(other)
+        return NotImplemented
+
+    __hash__ = None
+
+    @property
+    def real(self) -> np.ndarray:
+        return self.to_host().real
+
+    @property
+    def imag(self) -> np.ndarray:
+        return self.to_host().imag
+
+    def __repr__(self) -> str:
+        return f"DeviceArray(len={self.length}, dtype={self.dtype}, device={self.dctx.device})"
+
+    def free(self) -> None:
+        if self.ptr is not None and _lib is not None:
+            p, self.ptr = self.ptr, None
+            _lib.qsb_free(self.dctx.handle, p)
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

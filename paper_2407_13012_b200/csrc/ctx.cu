@@ -1,0 +1,291 @@
+// Context, memory and error plumbing of libqsb (the C ABI in include/qsb.h).
+#include <stdarg.h>
+#include <math.h>
+#include <string.h>
+
+#include "common.cuh"
+
+namespace {
+thread_local char g_err[1024] = "";
+}
+
+namespace qsb {
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error("CUDA error %s (%s) in %s", cudaGetErrorName(e), cudaGetErrorString(e), what);
+  if (e == cudaErrorMemoryAllocation) return QSB_ENOMEM;
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver || e == cudaErrorInvalidDevice)
+    return QSB_ENODEV;
+  return QSB_ECUDA;
+}
+
+int invalid(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return QSB_EINVAL;
+}
+
+int ensure_scratch(qsb_ctx* ctx, uint64_t bytes) {
+  if (bytes <= ctx->scratch_bytes) return QSB_OK;
+  if (ctx->d_scratch) {
+    QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    QSB_CUDA(cudaFree(ctx->d_scratch));
+    ctx->d_scratch = nullptr;
+    ctx->scratch_bytes = 0;
+  }
+  uint64_t want = bytes < (1u << 20) ? (1u << 20) : bytes;
+  QSB_CUDA(cudaMalloc(&ctx->d_scratch, want));
+  ctx->scratch_bytes = want;
+  return QSB_OK;
+}
+
+int ensure_small(qsb_ctx* ctx, uint64_t bytes) {
+  if (bytes <= ctx->small_bytes) return QSB_OK;
+  if (ctx->d_small) {
+    QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    QSB_CUDA(cudaFree(ctx->d_small));
+    ctx->d_small = nullptr;
+    ctx->small_bytes = 0;
+  }
+  uint64_t want = bytes < (1u << 16) ? (1u << 16) : bytes;
+  QSB_CUDA(cudaMalloc(&ctx->d_small, want));
+  ctx->small_bytes = want;
+  return QSB_OK;
+}
+
+int prof_mark(qsb_ctx* ctx, cudaEvent_t* ev) {
+  if (ctx->prof_used == ctx->prof_pool.size()) {
+    cudaEvent_t e;
+    QSB_CUDA(cudaEventCreate(&e));
+    ctx->prof_pool.push_back(e);
+  }
+  *ev = ctx->prof_pool[ctx->prof_used++];
+  QSB_CUDA(cudaEventRecord(*ev, ctx->stream));
+  return QSB_OK;
+}
+
+}  // namespace qsb
+
+using namespace qsb;
+
+extern "C" {
+
+const char* qsb_last_error(void) { return g_err; }
+int qsb_abi_version(void) { return 1; }
+
+int qsb_device_count(int* out) {
+  if (!out) return invalid("qsb_device_count: null out");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *out = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  *out = n;
+  return QSB_OK;
+}
+
+int qsb_ctx_create(int device, qsb_ctx** out) {
+  if (!out) return invalid("qsb_ctx_create: null out");
+  *out = nullptr;
+  QSB_CUDA(cudaSetDevice(device));
+  qsb_ctx* ctx = new qsb_ctx();
+  ctx->device = device;
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "cudaGetDeviceProperties"); }
+  if (prop.major < 10) {
+    delete ctx;
+    return invalid("device %d is sm_%d%d; libqsb is built for sm_100a (B200)", device, prop.major, prop.minor);
+  }
+  ctx->num_sms = prop.multiProcessorCount;
+  e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev1);
+  if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_small, 4096 * sizeof(double));
+  if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "context setup"); }
+  *out = ctx;
+  return QSB_OK;
+}
+
+int qsb_ctx_destroy(qsb_ctx* ctx) {
+  if (!ctx) return QSB_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->d_scratch) cudaFree(ctx->d_scratch);
+  if (ctx->d_small) cudaFree(ctx->d_small);
+  if (ctx->h_small) cudaFreeHost(ctx->h_small);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  for (cudaEvent_t e : ctx->prof_pool) cudaEventDestroy(e);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return QSB_OK;
+}
+
+int qsb_ctx_sync(qsb_ctx* ctx) {
+  if (!ctx) return invalid("null context");
+  QSB_CUDA(cudaSetDevice(ctx->device));
+  QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return QSB_OK;
+}
+
+int qsb_ctx_device(qsb_ctx* ctx, int* device) {
+  if (!ctx || !device) return invalid("null argument");
+  *device = ctx->device;
+  return QSB_OK;
+}
+
+int qsb_ctx_info(qsb_ctx* ctx, int* num_sms, uint64_t* free_bytes, uint64_t* total_bytes) {
+  if (!ctx) return invalid("null context");
+  QSB_CUDA(cudaSetDevice(ctx->device));
+  size_t f = 0, t = 0;
+  QSB_CUDA(cudaMemGetInfo(&f, &t));
+  if (num_sms) *num_sms = ctx->num_sms;
+  if (free_bytes) *free_bytes = f;
+  if (total_bytes) *total_bytes = t;
+  return QSB_OK;
+}
+
+int qsb_timer_start(qsb_ctx* ctx) {
+  if (!ctx) return invalid("null context");
+  QSB_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+  return QSB_OK;
+}
+
+int qsb_timer_stop(qsb_ctx* ctx, double* ms) {
+  if (!ctx || !ms) return invalid("null argument");
+  QSB_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+  QSB_CUDA(cudaEventSynchronize(ctx->ev1));
+  float f = 0;
+  QSB_CUDA(cudaEventElapsedTime(&f, ctx->ev0, ctx->ev1));
+  *ms = f;
+  return QSB_OK;
+}
+
+int qsb_prof_begin(qsb_ctx* ctx) {
+  if (!ctx) return invalid("null context");
+  ctx->prof = true;
+  ctx->prof_recs.clear();
+  ctx->prof_used = 0;
+  return QSB_OK;
+}
+
+// out[3*k + 0..2] = launches, total ms, algorithmic bytes for kernel kind k
+// (k = 0: single-vector sweep, 1: bra/ket sweep); nkinds entries are written.
+int qsb_prof_end(qsb_ctx* ctx, double* out, int nkinds) {
+  if (!ctx || !out) return invalid("null argument");
+  ctx->prof = false;
+  QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int k = 0; k < 3 * nkinds; ++k) out[k] = 0.0;
+  for (const auto& r : ctx->prof_recs) {
+    if (r.kind < 0 || r.kind >= nkinds) continue;
+    float ms = 0;
+    QSB_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    out[3 * r.kind] += 1.0;
+    out[3 * r.kind + 1] += ms;
+    out[3 * r.kind + 2] += r.bytes;
+  }
+  ctx->prof_recs.clear();
+  ctx->prof_used = 0;
+  return QSB_OK;
+}
+
+int qsb_ctx_xfer(qsb_ctx* ctx, uint64_t* h2d, uint64_t* d2h) {
+  if (!ctx) return invalid("null context");
+  if (h2d) *h2d = ctx->h2d_bytes;
+  if (d2h) *d2h = ctx->d2h_bytes;
+  return QSB_OK;
+}
+
+int qsb_ctx_launches(qsb_ctx* ctx, uint64_t* out) {
+  if (!ctx || !out) return invalid("null argument");
+  *out = ctx->launches;
+  return QSB_OK;
+}
+
+int qsb_alloc(qsb_ctx* ctx, uint64_t bytes, void** dptr) {
+  if (!ctx || !dptr) return invalid("null argument");
+  QSB_CUDA(cudaSetDevice(ctx->device));
+  *dptr = nullptr;
+  cudaError_t e = cudaMalloc(dptr, bytes ? bytes : 16);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error("device allocation of %llu bytes failed (%s)", (unsigned long long)bytes, cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? QSB_ENOMEM : QSB_ECUDA;
+  }
+  return QSB_OK;
+}
+
+int qsb_free(qsb_ctx* ctx, void* dptr) {
+  if (!ctx) return invalid("null context");
+  if (!dptr) return QSB_OK;
+  QSB_CUDA(cudaSetDevice(ctx->device));
+  // the buffer may still be in use by queued work on our stream
+  QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  QSB_CUDA(cudaFree(dptr));
+  return QSB_OK;
+}
+
+int qsb_h2d(qsb_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+  if (!ctx) return invalid("null context");
+  if (!bytes) return QSB_OK;
+  ctx->h2d_bytes += bytes;
+  QSB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return QSB_OK;
+}
+
+int qsb_d2h(qsb_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+  if (!ctx) return invalid("null context");
+  if (!bytes) return QSB_OK;
+  ctx->d2h_bytes += bytes;
+  QSB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return QSB_OK;
+}
+
+int qsb_h2d_async(qsb_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+  if (!ctx) return invalid("null context");
+  if (!bytes) return QSB_OK;
+  ctx->h2d_bytes += bytes;
+  QSB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return QSB_OK;
+}
+
+int qsb_d2h_async(qsb_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+  if (!ctx) return invalid("null context");
+  if (!bytes) return QSB_OK;
+  ctx->d2h_bytes += bytes;
+  QSB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  return QSB_OK;
+}
+
+int qsb_d2d(qsb_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+  if (!ctx) return invalid("null context");
+  if (!bytes) return QSB_OK;
+  QSB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  return QSB_OK;
+}
+
+int qsb_host_alloc(uint64_t bytes, void** hptr) {
+  if (!hptr) return invalid("null argument");
+  QSB_CUDA(cudaMallocHost(hptr, bytes ? bytes : 16));
+  return QSB_OK;
+}
+
+int qsb_host_free(void* hptr) {
+  if (hptr) QSB_CUDA(cudaFreeHost(hptr));
+  return QSB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,251 @@
+// Cost-table precompute (costpoly.precompute, costpoly.py:126-133 ->
+// numba_impl.precompute_table :229-238) and the compact index / phase LUT used
+// by the fused sweeps.
+//
+// T[x] = sum over terms k in the given order of w_k * [x & m_k == m_k], from 0.0.
+// One thread per 4 consecutive x (32-byte stores); a warp covers 128 consecutive
+// x, so a term whose mask has a bit >= 7 that is clear in the warp's common high
+// bits cannot match any x of the warp and is skipped warp-uniformly.  Skipping a
+// non-matching term is exactly what the reference does, so the sum is bit-exact
+// for any weights.
+#include <math.h>
+#include <string.h>
+
+#include "common.cuh"
+
+using namespace qsb;
+
+namespace {
+
+constexpr int kPreThreads = 256;
+constexpr int kPreX = 4;            // x values per thread
+constexpr int kTermChunk = 2048;    // terms staged in shared memory per pass
+
+__global__ void __launch_bounds__(kPreThreads) k_precompute(const double* __restrict__ w, const uint64_t* __restrict__ m,
+                                                            uint64_t num_terms, double* __restrict__ out, uint64_t len) {
+  __shared__ double sw[kTermChunk];
+  __shared__ uint64_t sm[kTermChunk];
+  const uint64_t x0 = ((uint64_t)blockIdx.x * kPreThreads + threadIdx.x) * kPreX;
+  // warp-common high bits (bits >= 7 are equal for all x of this warp)
+  const uint64_t warp_x = x0 & ~127ull;
+  double acc[kPreX];
+#pragma unroll
+  for (int e = 0; e < kPreX; ++e) acc[e] = 0.0;
+  for (uint64_t c0 = 0; c0 < num_terms; c0 += kTermChunk) {
+    const int cn = (int)((num_terms - c0) < (uint64_t)kTermChunk ? (num_terms - c0) : kTermChunk);
+    __syncthreads();
+    for (int i = threadIdx.x; i < cn; i += kPreThreads) {
+      sw[i] = w[c0 + i];
+      sm[i] = m[c0 + i];
+    }
+    __syncthreads();
+    for (int k = 0; k < cn; ++k) {
+      const uint64_t mk = sm[k];
+      if ((mk & ~127ull) & ~warp_x) continue;  // warp-uniform: no x in this warp matches
+      const double wk = sw[k];
+#pragma unroll
+      for (int e = 0; e < kPreX; ++e)
+        if (((x0 + e) & mk) == mk) acc[e] = __dadd_rn(acc[e], wk);
+    }
+  }
+  if (x0 + kPreX <= len) {
+    double2* o = (double2*)(out + x0);
+    o[0] = make_double2(acc[0], acc[1]);
+    o[1] = make_double2(acc[2], acc[3]);
+  } else {
+    for (int e = 0; e < kPreX; ++e)
+      if (x0 + e < len) out[x0 + e] = acc[e];
+  }
+}
+
+// compact index: idx = T - vmin when T is an integer; flags non-integral values
+template <typename IDX>
+__global__ void k_compact(const double* __restrict__ t, uint64_t len, double vmin, IDX* __restrict__ idx,
+                          int* __restrict__ bad) {
+  int local_bad = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (uint64_t)gridDim.x * blockDim.x) {
+    const double v = t[i];
+    const double d = v - vmin;
+    if (v != rint(v)) local_bad = 1;
+    idx[i] = (IDX)d;
+  }
+  if (__syncthreads_or(local_bad) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
+}  // namespace
+
+namespace qsb {
+
+int minmax(qsb_ctx* ctx, const double* v, uint64_t len, double* mn, double* mx);  // ops.cu
+
+static int precompute_into(qsb_ctx* ctx, const double* weights, const int64_t* masks, uint64_t num_terms,
+                           double* out, uint64_t len) {
+  const uint64_t tbytes = num_terms * (sizeof(double) + sizeof(uint64_t));
+  QSB_TRY(ensure_small(ctx, tbytes + 64));
+  double* dw = (double*)ctx->d_small;
+  uint64_t* dm = (uint64_t*)(dw + num_terms);
+  if (num_terms) {
+    // d_small may still be read by queued kernels -> synchronous, stream-ordered copies
+    QSB_CUDA(cudaMemcpyAsync(dw, weights, num_terms * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    QSB_CUDA(cudaMemcpyAsync(dm, masks, num_terms * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+  }
+  const uint64_t threads_needed = (len + kPreX - 1) / kPreX;
+  const uint64_t blocks = (threads_needed + kPreThreads - 1) / kPreThreads;
+  k_precompute<<<(unsigned)blocks, kPreThreads, 0, ctx->stream>>>(dw, dm, num_terms, out, len);
+  QSB_CHECK_LAUNCH(ctx, "precompute");
+  QSB_CUDA(cudaStreamSynchronize(ctx->stream));  // host term arrays / d_small reuse
+  return QSB_OK;
+}
+
+static int finish_table(qsb_ctx* ctx, qsb_table* t) {
+  QSB_TRY(minmax(ctx, t->values, t->len, &t->vmin, &t->vmax));
+  t->kind = 0;
+  t->nvals = 0;
+  const double range = t->vmax - t->vmin;
+  const bool integral_ends = t->vmin == rint(t->vmin) && t->vmax == rint(t->vmax) && fabs(t->vmin) < 1e15 &&
+                             fabs(t->vmax) < 1e15;
+  if (integral_ends && range < 65536.0) {
+    const int kind = range < 256.0 ? 1 : 2;
+    const size_t esz = kind == 1 ? 1 : 2;
+    void* idx = nullptr;
+    cudaError_t e = cudaMalloc(&idx, t->len * esz);
+    if (e != cudaSuccess) {  // compact table is an optimisation: fall back quietly
+      cudaGetLastError();
+      return QSB_OK;
+    }
+    QSB_TRY(ensure_scratch(ctx, 64));
+    int* bad = (int*)ctx->d_scratch;
+    QSB_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+    unsigned g = ctx->num_sms * 8;
+    if (kind == 1)
+      k_compact<uint8_t><<<g, 256, 0, ctx->stream>>>(t->values, t->len, t->vmin, (uint8_t*)idx, bad);
+    else
+      k_compact<uint16_t><<<g, 256, 0, ctx->stream>>>(t->values, t->len, t->vmin, (uint16_t*)idx, bad);
+    QSB_CHECK_LAUNCH(ctx, "compact");
+    int hbad = 0;
+    QSB_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hbad) {
+      cudaFree(idx);
+      return QSB_OK;
+    }
+    t->cidx = idx;
+    t->kind = kind;
+    t->nvals = (int)range + 1;
+    QSB_CUDA(cudaMalloc(&t->d_lut, (size_t)t->nvals * sizeof(double2)));
+    t->h_lutbuf.resize(2 * (size_t)t->nvals);
+  }
+  return QSB_OK;
+}
+
+// LUT entry k: extra * (cos(ang), sin(ang)), ang = ang_scale * (vmin + k), host libm
+// (glibc — the functions Python's math module and numba's math.cos/sin call).
+int upload_phase_lut(qsb_table* t, double ang_scale, double2 extra, bool exact) {
+  qsb_ctx* ctx = t->ctx;
+  double* h = t->h_lutbuf.data();
+  for (int k = 0; k < t->nvals; ++k) {
+    const double v = t->vmin + (double)k;
+    const double ang = ang_scale * v;
+    double c = cos(ang), s = sin(ang);
+    if (!exact) {
+      const double c2 = c * extra.x - s * extra.y;
+      const double s2 = c * extra.y + s * extra.x;
+      c = c2;
+      s = s2;
+    }
+    h[2 * k] = c;
+    h[2 * k + 1] = s;
+  }
+  // the previous LUT may still be read by a queued sweep: order on the stream,
+  // and wait so the host staging buffer can be rewritten safely next time
+  QSB_CUDA(cudaMemcpyAsync(t->d_lut, h, (size_t)t->nvals * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+  QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return QSB_OK;
+}
+
+int launch_phase_lut(qsb_ctx* ctx, qsb_table* t, double2* amps);  // ops.cu
+
+}  // namespace qsb
+
+extern "C" {
+
+int qsb_precompute_table(qsb_ctx* ctx, const double* weights, const int64_t* masks, uint64_t num_terms,
+                         double* out, uint64_t len) {
+  if (!ctx || !out || (num_terms && (!weights || !masks))) return invalid("qsb_precompute_table: null argument");
+  if (!len) return QSB_OK;
+  return precompute_into(ctx, weights, masks, num_terms, out, len);
+}
+
+int qsb_table_create(qsb_ctx* ctx, int n, const double* weights, const int64_t* masks, uint64_t num_terms,
+                     double* values, double* min_out, double* max_out, qsb_table** out) {
+  if (!ctx || !values || !out) return invalid("qsb_table_create: null argument");
+  if (n < 1 || n > 62) return invalid("qsb_table_create: n=%d out of range", n);
+  const uint64_t len = 1ull << n;
+  for (uint64_t k = 0; k < num_terms; ++k)
+    if (masks[k] < 0 || (uint64_t)masks[k] >= len) return invalid("term mask %lld out of range for n=%d", (long long)masks[k], n);
+  QSB_TRY(precompute_into(ctx, weights, masks, num_terms, values, len));
+  return qsb_table_wrap(ctx, n, values, min_out, max_out, out);
+}
+
+int qsb_table_wrap(qsb_ctx* ctx, int n, double* values, double* min_out, double* max_out, qsb_table** out) {
+  if (!ctx || !values || !out) return invalid("qsb_table_wrap: null argument");
+  if (n < 1 || n > 62) return invalid("qsb_table_wrap: n=%d out of range", n);
+  qsb_table* t = new qsb_table();
+  t->ctx = ctx;
+  t->n = n;
+  t->len = 1ull << n;
+  t->values = values;
+  int rc = finish_table(ctx, t);
+  if (rc != QSB_OK) {
+    qsb_table_destroy(t);
+    return rc;
+  }
+  if (min_out) *min_out = t->vmin;
+  if (max_out) *max_out = t->vmax;
+  *out = t;
+  return QSB_OK;
+}
+
+int qsb_table_destroy(qsb_table* t) {
+  if (!t) return QSB_OK;
+  if (t->ctx) {
+    cudaSetDevice(t->ctx->device);
+    cudaStreamSynchronize(t->ctx->stream);
+  }
+  if (t->cidx) cudaFree(t->cidx);
+  if (t->d_lut) cudaFree(t->d_lut);
+  delete t;
+  return QSB_OK;
+}
+
+int qsb_table_kind(qsb_table* t, int* kind, int* num_values) {
+  if (!t) return invalid("null table");
+  if (kind) *kind = t->kind;
+  if (num_values) *num_values = t->nvals;
+  return QSB_OK;
+}
+
+// Phase multiply through a table object: exact LUT path when compact
+// (bit-identical to numba's glibc cos/sin), device sincos otherwise.
+int qsb_table_phase(qsb_ctx* ctx, qsb_table* t, double* amps, double gamma) {
+  if (!ctx || !t || !amps) return invalid("qsb_table_phase: null argument");
+  if (t->kind == 0) {
+    extern int qsb_phase_by_table(qsb_ctx*, double*, const double*, uint64_t, double);
+    return qsb_phase_by_table(ctx, amps, t->values, t->len, gamma);
+  }
+  QSB_TRY(upload_phase_lut(t, -gamma, make_double2(1.0, 0.0), true));
+  return launch_phase_lut(ctx, t, (double2*)amps);
+}
+
+// Host-only helper (no device needed): the LUT the library would build, for tests.
+int qsb_phase_lut_host(double gamma, double vmin, int nvals, double* out) {
+  if (!out || nvals < 0) return invalid("qsb_phase_lut_host: bad argument");
+  for (int k = 0; k < nvals; ++k) {
+    const double ang = (-gamma) * (vmin + (double)k);
+    out[2 * k] = cos(ang);
+    out[2 * k + 1] = sin(ang);
+  }
+  return QSB_OK;
+}
+
+}  // extern "C"

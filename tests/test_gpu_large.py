@@ -1,0 +1,70 @@
+"""Full-size BASELINE configs on one B200.
+
+C3 (MaxCut 3-regular n=30 p=6, E + full gradient + 10^6 shots) is compared with
+the golden values the reference produced in the survey container (BASELINE.md
+section 3, numba, 771 s on 8 cores): cost table sha256 bit-exact, expectation and
+gradient within 1e-10 (norm-wise, the last d_gamma is structurally ~1e-16).
+Size-independent properties cover what no CPU oracle reaches in seconds."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_2407_13012_b200 as qs
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+C3_TABLE_SHA = "3d901e9fb11f654bea686c8b5fc4c3abe78610bc2db777d6253d40fbab2c8940"
+C3_E = -34.826219584831264
+C3_DG = [2.0196252857797266, 0.5485729644673372, -3.64045246150112, -2.7503754175554738, 0.07157226648264126, 0.0]
+C3_DB = [-1.253325295745509, 0.3693458471178387, 5.082754776288641, -3.7670124001326, -4.11054167260661,
+         -12.47191716563579]
+
+
+@pytest.fixture(scope="module")
+def c3():
+    poly = qs.maxcut_polynomial(qs.random_regular(30, 3, seed=1))
+    h = qs.create_handle(poly, backend_name="b200")
+    yield poly, h
+    h.close()
+
+
+def test_c3_table_bit_exact(c3):
+    poly, h = c3
+    t = h.table.values.data.to_host()
+    assert hashlib.sha256(t.tobytes()).hexdigest() == C3_TABLE_SHA
+    assert (h.table.min_value, h.table.max_value) == (-40.0, 0.0)
+    del t
+
+
+@pytest.mark.parametrize("exact", ["0", "1"])
+def test_c3_expectation_and_gradient(c3, monkeypatch, exact):
+    monkeypatch.setenv("QAOA_B200_EXACT", exact)
+    poly, h = c3
+    params = qs.linear_ramp_params(6)
+    e = qs.expectation(h, params)
+    assert abs(e - C3_E) <= 1e-10 * abs(C3_E)
+    if exact == "1":
+        assert e == C3_E
+    v, g = qs.value_and_grad(h, params)
+    assert abs(v - C3_E) <= 1e-10 * abs(C3_E)
+    got = np.array(list(g.d_gammas) + list(g.d_betas))
+    want = np.array(C3_DG + C3_DB)
+    assert np.max(np.abs(got - want)) <= 1e-10 * np.max(np.abs(want))
+    assert abs(g.d_gammas[-1]) < 1e-12  # beta_p = 0 makes the last d_gamma vanish
+
+
+def test_c3_norm_and_million_shots(c3):
+    poly, h = c3
+    params = qs.linear_ramp_params(6)
+    qs.simulate(h, params)
+    ss = qs.draw(h, 1_000_000, 1)
+    assert ss.indices.shape == (1_000_000,)
+    # costs are the table entries, which equal the scalar objective
+    for b, c in list(zip(ss.indices[:200].tolist(), ss.costs[:200].tolist())):
+        assert c == qs.evaluate(poly, b)
+    # sample mean of the cost estimates <C> (std of C <= 40 -> 6-sigma ~ 0.24)
+    assert abs(ss.costs.mean() - C3_E) < 0.25
+    again = qs.draw(h, 1000, 1)
+    assert np.array_equal(again.indices, ss.indices[:1000])
