@@ -359,6 +359,11 @@ def run_b200(args, rank: int, world: int, dist) -> None:
             "launches_per_step": n_l / args.steps,
             "alg_bytes_per_launch": b / n_l,
         },
+        "kernels": {
+            k: {"launches_per_step": v[0] / args.steps, "ms_per_step": v[1] / args.steps,
+                "gbs": v[2] / (v[1] * 1e-3) / 1e9, "frac": v[2] / (v[1] * 1e-3) / 1e9 / peaks["hbm_gbs"]}
+            for k, v in kinds.items()
+        },
         "sweeps_share_of_step": total_sweep_ms / ms,
         "step_hbm_gbs": all_bytes / (ms * 1e-3) / 1e9,
         "e2e": {

@@ -300,7 +300,8 @@ class DeviceArray:
     def free(self) -> None:
         if self.ptr is not None and _lib is not None:
             p, self.ptr = self.ptr, None
-            _lib.qsb_free(self.dctx.handle, p)
+            # the context may already be gone (cyclic GC order): free without it
+            _lib.qsb_free(None if self.dctx._closed else self.dctx.handle, p)
 
     def __del__(self):
         try:

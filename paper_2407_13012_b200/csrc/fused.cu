@@ -28,33 +28,6 @@ extern "C" int qsb_diag_scale(qsb_ctx* ctx, double* amps, const double* table, u
 namespace {
 
 // ------------------------------------------------------------------ planning
-struct PhaseSpec {
-  int lanes[5];
-  int warps[4];
-  int reg_l;
-  bool allow;
-};
-
-// local-bit layouts (see sweep.cu); each row is a partition of local bits 0..11
-const PhaseSpec kA1Fast[] = {{{0, 1, 2, 3, 4}, {5, 6}, 7, true},
-                             {{5, 6, 7, 8, 9}, {10, 11}, 0, true},
-                             {{0, 1, 2, 3, 4}, {10, 11}, 5, true}};
-const PhaseSpec kA1Exact[] = {{{0, 1, 2, 3, 4}, {5, 6}, 7, false},
-                              {{5, 6, 7, 8, 9}, {10, 11}, 0, true},
-                              {{0, 1, 2, 3, 4}, {10, 11}, 5, true},
-                              {{0, 1, 2, 3, 4}, {5, 6}, 7, true}};
-const PhaseSpec kB1[] = {{{0, 1, 2, 8, 9}, {10, 11}, 3, true}, {{0, 1, 2, 3, 4}, {5, 6}, 7, true}};
-const PhaseSpec kA2Fast[] = {{{0, 1, 2, 3, 4}, {5, 6, 7}, 8, true},
-                             {{4, 5, 6, 7, 8}, {9, 10, 11}, 0, true},
-                             {{0, 1, 2, 3, 8}, {9, 10, 11}, 4, true}};
-const PhaseSpec kA2Exact[] = {{{0, 1, 2, 3, 4}, {5, 6, 7}, 8, false},
-                              {{4, 5, 6, 7, 8}, {9, 10, 11}, 0, true},
-                              {{0, 1, 2, 3, 8}, {9, 10, 11}, 4, true},
-                              {{0, 1, 2, 3, 4}, {5, 6, 7}, 8, true}};
-const PhaseSpec kB2[] = {{{0, 1, 2, 7, 8}, {9, 10, 11}, 3, true},
-                         {{0, 1, 2, 3, 4}, {9, 10, 11}, 5, true},
-                         {{0, 1, 2, 3, 4}, {5, 6, 7}, 8, true}};
-
 struct SweepShape {
   bool is_a;
   int lo;      // first target qubit
@@ -76,25 +49,12 @@ std::vector<SweepShape> plan_sweeps(int n) {
 int build_shape(const SweepShape& sh, int n, int nv, bool exact, SweepArgs& a, int gates_before_phase[kMaxPhases]) {
   int gl[kSweepT];
   for (int i = 0; i < kSweepT; ++i) gl[i] = sh.is_a ? i : (i < 3 ? i : sh.glo + i - 3);
-  const PhaseSpec* ps;
-  int np;
-  if (nv == 1) {
-    if (sh.is_a) {
-      ps = exact ? kA1Exact : kA1Fast;
-      np = exact ? 4 : 3;
-    } else {
-      ps = kB1;
-      np = 2;
-    }
-  } else {
-    if (sh.is_a) {
-      ps = exact ? kA2Exact : kA2Fast;
-      np = exact ? 4 : 3;
-    } else {
-      ps = kB2;
-      np = 3;
-    }
-  }
+  const int shape = pick_shape(nv, exact, sh.is_a);
+  const int np = shape_np(shape);
+  PhaseSpec ps[kMaxPhases];
+  for (int p = 0; p < np; ++p) ps[p] = shape_phase(shape, p);
+  a.shape = shape;
+  a.glo = sh.is_a ? 3 : sh.glo;
   const int R = nv == 1 ? 5 : 4;
   const int W = nv == 1 ? 2 : 3;
   bool applied[kSweepT] = {false};
@@ -127,6 +87,24 @@ int build_shape(const SweepShape& sh, int n, int nv, bool exact, SweepArgs& a, i
     }
     m.apply = apply;
   }
+  // cp.async load mapping: lanes <-> local 0..4, warps <-> next W bits, R register bits on top
+  {
+    PhaseMap& m = a.ld;
+    memset(&m, 0, sizeof(m));
+    for (int b = 0; b < 5; ++b) {
+      m.lane_l[b] = (uint8_t)b;
+      m.lane_g[b] = (uint8_t)gl[b];
+    }
+    for (int b = 0; b < W; ++b) {
+      m.warp_l[b] = (uint8_t)(5 + b);
+      m.warp_g[b] = (uint8_t)gl[5 + b];
+    }
+    m.reg_l = (uint8_t)(5 + W);
+    m.reg_g = (uint8_t)gl[5 + W];
+    for (int b = 0; b < R; ++b)
+      if (gl[5 + W + b] != gl[5 + W] + b) return -1;
+  }
+  a.cshift = gl[3];
   // tile index -> global base: the non-tile bits as contiguous runs
   a.nruns = 0;
   auto add_run = [&](int pos, int len) {
@@ -302,6 +280,10 @@ struct Runner {
     if (gates < 0) return invalid("internal: bad sweep layout");
     a.v0 = v0;
     a.v1 = v1;
+    if (!sh.is_a) {  // TMA boxes for the strided B tiles
+      QSB_TRY(encode_b_tile_map(&a.tm0, v0, n, sh.glo));
+      if (nv == 2) QSB_TRY(encode_b_tile_map(&a.tm1, v1, n, sh.glo));
+    }
     set_table(a, t);
     a.lut = lut;
     a.pre_ang = pre_ang;
@@ -536,7 +518,9 @@ int qsb_value_and_grad(qsb_ctx* ctx, qsb_table* t, double* ket_, double* bra_, i
     double xs = 0.0;
     for (int sw : xs_sweeps[i]) xs += Runner::slot_sum(h, R.maxgrid, R.grids, sw, 2);
     d_betas[i] = -2.0 * xs;
-    d_gammas[i] = 2.0 * Runner::slot_sum(h, R.maxgrid, R.grids, dg_sweep[i], 1);
+    // layer 0's contraction comes from the last sweep's post op (slot 0), the
+    // others from the next layer group's first sweep (slot 1)
+    d_gammas[i] = 2.0 * Runner::slot_sum(h, R.maxgrid, R.grids, dg_sweep[i], i == 0 ? 0 : 1);
   }
   if (value) {
     if (esweep >= 0) *value = Runner::slot_sum(h, R.maxgrid, R.grids, esweep, 0);

@@ -1,13 +1,15 @@
 // Fused multi-qubit sweep: descriptor shared by the kernel (sweep.cu) and the
 // host-side planner / orchestration (fused.cu).
 #pragma once
+#include <cuda.h>  // CUtensorMap (TMA descriptors; encoded through the runtime driver entry point)
+
 #include "common.cuh"
 
 namespace qsb {
 
 constexpr int kSweepT = 12;        // tile = 2^12 amplitudes per vector
 constexpr int kMaxPhases = 4;
-constexpr int kSlots = 3;          // partial-sum slots: 0 expectation, 1 diag inner, 2 xsum
+constexpr int kSlots = 3;          // partial-sum slots: 0 expectation / post diag inner, 1 pre diag inner, 2 xsum
 
 enum SweepFlags : uint32_t {
   SF_PLUS = 1u << 0,         // input is |+> (not loaded)
@@ -16,7 +18,7 @@ enum SweepFlags : uint32_t {
   SF_PRE_DINNER = 1u << 3,   // NV=2: slot1 += T*Im(conj(bra) ket) at load, before the phase
   SF_XSUM = 1u << 4,         // NV=2: slot2 += w_phase * Im sum_pairs conj(b)X k, before each gate
   SF_POST_EXPECT = 1u << 5,  // NV=1: slot0 += T*|psi|^2 after gates and post scale
-  SF_POST_DINNER = 1u << 6,  // NV=2: slot1 += T*Im(conj(bra) ket) after gates and post scale
+  SF_POST_DINNER = 1u << 6,  // NV=2: slot0 += T*Im(conj(bra) ket) after gates and post scale
   SF_NO_STORE = 1u << 7,
   SF_POST_SCALE = 1u << 8,   // multiply by the real post_scale after the gates
 };
@@ -37,6 +39,7 @@ struct PhaseMap {
 };
 
 struct SweepArgs {
+  CUtensorMap tm0, tm1;   // B shapes: 5-D TMA boxes over v0 / v1 (one 64 KB tile per load)
   double2* v0;            // ket / the single vector
   double2* v1;            // bra (NV=2)
   const void* cidx;       // compact table index (kind 1: u8, 2: u16)
@@ -58,11 +61,69 @@ struct SweepArgs {
   int nphase;
   int nruns;
   uint8_t run_pos[4], run_len[4];
+  int cshift;             // global bit of local bit 3 (cidx 8-entry chunk c -> base + (c << cshift))
+  int shape;              // SweepShapeId
+  int glo;                // B shapes: global bit of local bit 3
+  PhaseMap ld;            // cp.async load mapping: lanes <-> local 0..4 (coalesced)
   PhaseMap ph[kMaxPhases];
 };
 
-// launch one sweep (picks the instantiation); grid chosen from occupancy
+// ---------------------------------------------------------------- sweep shapes
+// A shape is the compile-time list of phase mappings of the 12 local bits onto
+// (5 lane bits, W warp bits, R consecutive register bits).  Shapes 0-2 are the
+// single-vector kernels (R=5, W=2), 3-5 the bra/ket kernels (R=4, W=3).
+// "A" shapes: local bit i == global bit i (contiguous 4096-amplitude tiles).
+// "B" shapes: local 0..2 -> global 0..2, local 3+i -> global glo+i.
+// `allow` = false marks a load-only phase (exact mode keeps ascending order).
+struct PhaseSpec {
+  int lanes[5];
+  int warps[4];
+  int reg_l;
+  bool allow;
+};
+
+enum SweepShapeId : int { SH_A1 = 0, SH_A1X = 1, SH_B1 = 2, SH_A2 = 3, SH_A2X = 4, SH_B2 = 5 };
+
+__host__ __device__ constexpr int shape_np(int sh) {
+  return sh == SH_A1 ? 3 : sh == SH_A1X ? 4 : sh == SH_B1 ? 2 : sh == SH_A2 ? 3 : sh == SH_A2X ? 4 : 3;
+}
+__host__ __device__ constexpr bool shape_is_a(int sh) { return sh != SH_B1 && sh != SH_B2; }
+__host__ __device__ constexpr int shape_r(int sh) { return sh <= SH_B1 ? 5 : 4; }
+__host__ __device__ constexpr int shape_w(int sh) { return sh <= SH_B1 ? 2 : 3; }
+
+__host__ __device__ constexpr PhaseSpec shape_phase(int sh, int p) {
+  // clang-format off
+  return sh == SH_A1 ? (p == 0 ? PhaseSpec{{0, 1, 2, 3, 4}, {5, 6, 0, 0}, 7, true}
+                      : p == 1 ? PhaseSpec{{5, 6, 7, 8, 9}, {10, 11, 0, 0}, 0, true}
+                      :          PhaseSpec{{0, 1, 2, 3, 4}, {10, 11, 0, 0}, 5, true})
+       : sh == SH_A1X ? (p == 0 ? PhaseSpec{{0, 1, 2, 3, 4}, {5, 6, 0, 0}, 7, false}
+                      : p == 1 ? PhaseSpec{{5, 6, 7, 8, 9}, {10, 11, 0, 0}, 0, true}
+                      : p == 2 ? PhaseSpec{{0, 1, 2, 3, 4}, {10, 11, 0, 0}, 5, true}
+                      :          PhaseSpec{{0, 1, 2, 3, 4}, {5, 6, 0, 0}, 7, true})
+       : sh == SH_B1 ? (p == 0 ? PhaseSpec{{0, 1, 2, 8, 9}, {10, 11, 0, 0}, 3, true}
+                      :          PhaseSpec{{0, 1, 2, 3, 4}, {5, 6, 0, 0}, 7, true})
+       : sh == SH_A2 ? (p == 0 ? PhaseSpec{{0, 1, 2, 3, 4}, {5, 6, 7, 0}, 8, true}
+                      : p == 1 ? PhaseSpec{{4, 5, 6, 7, 8}, {9, 10, 11, 0}, 0, true}
+                      :          PhaseSpec{{0, 1, 2, 3, 8}, {9, 10, 11, 0}, 4, true})
+       : sh == SH_A2X ? (p == 0 ? PhaseSpec{{0, 1, 2, 3, 4}, {5, 6, 7, 0}, 8, false}
+                      : p == 1 ? PhaseSpec{{4, 5, 6, 7, 8}, {9, 10, 11, 0}, 0, true}
+                      : p == 2 ? PhaseSpec{{0, 1, 2, 3, 8}, {9, 10, 11, 0}, 4, true}
+                      :          PhaseSpec{{0, 1, 2, 3, 4}, {5, 6, 7, 0}, 8, true})
+       :                (p == 0 ? PhaseSpec{{0, 1, 2, 7, 8}, {9, 10, 11, 0}, 3, true}
+                      : p == 1 ? PhaseSpec{{0, 1, 2, 3, 4}, {9, 10, 11, 0}, 5, true}
+                      :          PhaseSpec{{0, 1, 2, 3, 4}, {5, 6, 7, 0}, 8, true});
+  // clang-format on
+}
+
+__host__ __device__ constexpr int pick_shape(int nv, bool exact, bool is_a) {
+  return nv == 1 ? (is_a ? (exact ? SH_A1X : SH_A1) : SH_B1) : (is_a ? (exact ? SH_A2X : SH_A2) : SH_B2);
+}
+
+// launch one sweep (picks the instantiation from a.shape / a.form / a.kind);
+// B shapes need tm0 (and tm1 for NV=2) encoded with encode_b_tile_map()
 int launch_sweep(qsb_ctx* ctx, int nv, bool exact, SweepArgs& a, unsigned* grid_out);
+// 5-D box over a statevector for a B-shape tile with local bit 3 at global bit glo
+int encode_b_tile_map(CUtensorMap* map, const double2* base, int n, int glo);
 int sweep_grid(qsb_ctx* ctx, int nv, bool exact, uint64_t ntiles, unsigned* grid_out);
 
 }  // namespace qsb

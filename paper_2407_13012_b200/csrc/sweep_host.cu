@@ -1,0 +1,67 @@
+// Host side of the fused sweep: kernel dispatch and TMA descriptor encoding.
+#include <string.h>
+
+#include "sweep.cuh"
+
+namespace qsb {
+
+int launch_sweep_nv1(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int launch_sweep_nv2(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int grid_sweep_nv1(qsb_ctx* ctx, SweepArgs& a, uint64_t ntiles, unsigned* g);
+int grid_sweep_nv2(qsb_ctx* ctx, SweepArgs& a, uint64_t ntiles, unsigned* g);
+
+int launch_sweep(qsb_ctx* ctx, int nv, bool exact, SweepArgs& a, unsigned* gout) {
+  (void)exact;  // a.shape / a.form carry the choice
+  return nv == 1 ? launch_sweep_nv1(ctx, a, gout) : launch_sweep_nv2(ctx, a, gout);
+}
+
+int sweep_grid(qsb_ctx* ctx, int nv, bool exact, uint64_t ntiles, unsigned* g) {
+  // all shapes run one persistent CTA per SM; query the A-shape instantiation
+  SweepArgs a;
+  memset(&a, 0, sizeof(a));
+  a.shape = pick_shape(nv, exact, true);
+  a.form = exact ? GF_EXACT : GF_FACT_C;
+  a.kind = 1;
+  return nv == 1 ? grid_sweep_nv1(ctx, a, ntiles, g) : grid_sweep_nv2(ctx, a, ntiles, g);
+}
+
+namespace {
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+}  // namespace
+
+// B tile: local bits 0..2 -> global 0..2 (8 amplitudes = 16 doubles, 128 B), local
+// 3..7 -> glo..glo+4, local 8..11 -> glo+5..glo+8.  As a 5-D tensor of doubles
+// (innermost first): {16, 2^(glo-3), 32, 16, 2^(n-glo-9)}; box {16, 1, 32, 16, 1}
+// lands one 64 KB tile in local-index order.
+int encode_b_tile_map(CUtensorMap* map, const double2* base, int n, int glo) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return invalid("cuTensorMapEncodeTiled unavailable (driver too old?)");
+  if (glo < 3 || n - glo - 9 < 0) return invalid("internal: bad B tile geometry n=%d glo=%d", n, glo);
+  const cuuint64_t dims[5] = {16, 1ull << (glo - 3), 32, 16, 1ull << (n - glo - 9)};
+  const cuuint64_t strides[4] = {128, (1ull << glo) * 16, (1ull << (glo + 5)) * 16, (1ull << (glo + 9)) * 16};
+  const cuuint32_t box[5] = {16, 1, 32, 16, 1};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return invalid("cuTensorMapEncodeTiled failed (%d) for n=%d glo=%d", (int)r, n, glo);
+  return QSB_OK;
+}
+
+}  // namespace qsb

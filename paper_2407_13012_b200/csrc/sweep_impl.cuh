@@ -1,0 +1,462 @@
+// The fused sweep kernel — the hot path of every forward and backward layer.
+// (Instantiated in sweep_nv1.cu / sweep_nv2.cu; descriptor in sweep.cuh.)
+//
+// One launch streams the whole statevector (or the bra/ket pair) through HBM once.
+// A CTA owns 2^12-amplitude tiles whose 12 "local" bits map to global index bits
+// (shape "A": bits 0..11, contiguous; shape "B": bits 0..2 for 128-byte runs plus
+// 9 higher bits glo..glo+8).  Each thread keeps 2^R amplitudes per vector in
+// registers; a phase maps the 12 local bits onto (5 lane bits, W warp bits, R
+// register bits), fixed at compile time by the shape, so shared-memory addresses
+// are `thread_base (+|^) constant`.  Butterflies for register bits run in
+// registers; between phases the tile is re-mapped through an XOR-swizzled
+// shared-memory exchange (conflict-free 16-byte accesses: quarter-warp lanes
+// always sit on three consecutive local bits, whose swizzle images are
+// independent).
+//
+// Data movement is Blackwell-native: the kernel is persistent (one CTA per SM)
+// and one elected thread streams vector-tiles into a ring of three 64 KB
+// shared-memory slots with TMA — a single 1-D cp.async.bulk for a contiguous A
+// tile, a single 5-D cp.async.bulk.tensor box for a strided B tile — completing
+// on per-slot mbarriers (expect_tx).  While a tile is transformed in registers
+// the next one or two vector-tiles are in flight (128 KB per SM).  The landed
+// tile is read in the natural layout (every shape's first phase puts quarter-warp
+// lanes on local bits 0..2: conflict-free), exchanges use the swizzled layout,
+// and results go straight from registers to HBM with coalesced 16-byte stores.
+//
+// Fused ops: the cost phase exp(-i*gamma*C) (compact index -> LUT, the index tile
+// rides the A-tile TMA), bra = C*ket, <bra|C|ket>, sum_j <bra|X_j|ket> (before each
+// phase's gates) and <psi|C|psi>.
+#pragma once
+#include "sweep.cuh"
+
+namespace qsb {
+namespace sweepk {
+
+using namespace qsbd;
+
+constexpr int kRing = 3;  // shared-memory slots (one vector-tile each)
+constexpr uint32_t kTile = 1u << kSweepT;
+constexpr uint32_t kSlotBytes = kTile * 16u;
+constexpr uint32_t kCBytes = kTile * 2u;  // compact-index slot (u16 worst case)
+constexpr size_t kSmemBytes = (size_t)kRing * kSlotBytes + (size_t)kRing * kCBytes + 256 * 16 + 64;
+
+__host__ __device__ constexpr uint32_t swz(uint32_t x) {
+  return x ^ (((x >> 3) ^ (x >> 6) ^ (x >> 9) ^ (x >> 12)) & 7u);
+}
+
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ double2 lds(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts(uint32_t addr, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_1d(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tma_5d(uint32_t dst, const CUtensorMap* map, int c1, int c4, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+      "%6}], [%7];" ::"r"(dst),
+      "l"(map), "r"(0), "r"(c1), "r"(0), "r"(0), "r"(c4), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ uint64_t tile_base(const SweepArgs& a, uint64_t tile) {
+  uint64_t base = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    if (r < a.nruns) {
+      base |= (tile & ((1ull << a.run_len[r]) - 1ull)) << a.run_pos[r];
+      tile >>= a.run_len[r];
+    }
+  }
+  return base;
+}
+
+// global offset (in amplitudes) of local index l
+template <bool IS_A>
+__device__ __forceinline__ uint64_t gofs(uint32_t l, int glo) {
+  if constexpr (IS_A) return l;
+  else return (uint64_t)(l & 7u) | ((uint64_t)(l >> 3) << glo);
+}
+
+// local index of this thread's register-0 amplitude under phase map P
+template <int W>
+__device__ __forceinline__ uint32_t lbase(const PhaseSpec P, int lane, int warp) {
+  uint32_t lb = 0;
+#pragma unroll
+  for (int b = 0; b < 5; ++b) lb |= ((uint32_t)(lane >> b) & 1u) << P.lanes[b];
+#pragma unroll
+  for (int b = 0; b < W; ++b) lb |= ((uint32_t)(warp >> b) & 1u) << P.warps[b];
+  return lb;
+}
+
+template <int FORM>
+__device__ __forceinline__ void butterfly(double2& t, double2& u, double ga, double gb) {
+  if constexpr (FORM == GF_EXACT) {  // numba_impl.py:60-72, products rounded separately
+    const double c = ga, s = gb;
+    const double2 n0 = make_double2(__dadd_rn(__dmul_rn(c, t.x), __dmul_rn(s, u.y)),
+                                    __dadd_rn(__dmul_rn(c, t.y), -__dmul_rn(s, u.x)));
+    const double2 n1 = make_double2(__dadd_rn(__dmul_rn(s, t.y), __dmul_rn(c, u.x)),
+                                    __dadd_rn(__dmul_rn(c, u.y), -__dmul_rn(s, t.x)));
+    t = n0;
+    u = n1;
+  } else if constexpr (FORM == GF_FACT_C) {  // (a, b) = (1, tau): 4 FMA per pair
+    const double2 n0 = make_double2(fma(gb, u.y, t.x), fma(-gb, u.x, t.y));
+    const double2 n1 = make_double2(fma(gb, t.y, u.x), fma(-gb, t.x, u.y));
+    t = n0;
+    u = n1;
+  } else {  // (a, b) = (rho, 1)
+    const double2 n0 = make_double2(fma(ga, t.x, u.y), fma(ga, t.y, -u.x));
+    const double2 n1 = make_double2(fma(ga, u.x, t.y), fma(ga, u.y, -t.x));
+    t = n0;
+    u = n1;
+  }
+}
+
+// ------------------------------------------------------------------ kernel
+// SH: shape, NV: vectors (1 or 2), FORM: gate arithmetic, KSIN: f64 table +
+// device sincos for the A-shape pre ops (else compact index + LUT).
+template <int SH, int NV, int FORM, bool KSIN>
+__global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_constant__ SweepArgs a) {
+  constexpr int R = shape_r(SH), W = shape_w(SH), NP = shape_np(SH);
+  constexpr bool IS_A = shape_is_a(SH);
+  constexpr bool EXACT = FORM == GF_EXACT;
+  constexpr int NT = 32 << W;
+  constexpr int NR = 1 << R;
+  static_assert(5 + W + R == kSweepT, "tile size");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(smem_raw);
+  const uint32_t cring_s = ring_s + kRing * kSlotBytes;
+  uint8_t* cring = smem_raw + kRing * kSlotBytes;
+  double2* slut = (double2*)(cring + kRing * kCBytes);
+  const uint32_t bar_s = ring_s + kRing * kSlotBytes + kRing * kCBytes + 256 * 16;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t flags = a.flags;
+  const int glo = a.glo;
+  // compact-index tiles ride the A-tile TMA (B shapes read the table from HBM)
+  const bool cidx_tma = IS_A && !KSIN && a.kind != 0 &&
+                        (flags & (SF_PRE_PHASE | SF_BRA_FROM_KET | SF_PRE_DINNER | SF_POST_EXPECT | SF_POST_DINNER));
+  const uint32_t cbytes = a.kind == 2 ? 2u * kTile : kTile;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < kRing; ++s) mbar_init(bar_s + 8 * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (!KSIN && a.kind == 1 && (flags & SF_PRE_PHASE)) {
+    for (int i = threadIdx.x; i < a.nlut; i += NT) slut[i] = a.lut[i];
+  }
+  __syncthreads();
+
+  const uint64_t my_tiles = a.ntiles > blockIdx.x ? (a.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const uint64_t nseq = my_tiles * NV;
+
+  // producer (thread 0): sequence s -> slot s % 3.  NV=1: tile s; NV=2: even = bra
+  // (v1) of tile s/2, odd = ket (v0).
+  auto issue = [&](uint64_t s) {
+    if (threadIdx.x != 0 || s >= nseq) return;
+    const uint64_t k = s / NV;
+    const int q = NV == 2 ? (int)((s & 1) ^ 1) : 0;
+    const uint64_t tile = blockIdx.x + k * gridDim.x;
+    const uint32_t slot = (uint32_t)(s % kRing);
+    const uint32_t bar = bar_s + 8 * slot;
+    const bool vec = !((q == 0 && (flags & SF_PLUS)) || (q == 1 && (flags & SF_BRA_FROM_KET)));
+    const bool cid = cidx_tma && (s % NV) == 0;
+    const uint32_t bytes = (vec ? kSlotBytes : 0u) + (cid ? cbytes : 0u);
+    if (bytes == 0) {
+      mbar_arrive(bar);
+      return;
+    }
+    mbar_expect_tx(bar, bytes);
+    if (vec) {
+      if constexpr (IS_A) {
+        const uint64_t base = tile << kSweepT;
+        tma_1d(ring_s + slot * kSlotBytes, (q == 0 ? a.v0 : a.v1) + base, kSlotBytes, bar);
+      } else {
+        const int lowbits = glo - 3;
+        const int c1 = (int)(tile & ((1ull << lowbits) - 1ull));
+        const int c4 = (int)(tile >> lowbits);
+        tma_5d(ring_s + slot * kSlotBytes, q == 0 ? &a.tm0 : &a.tm1, c1, c4, bar);
+      }
+    }
+    if (cid) {
+      const uint64_t base = tile << kSweepT;
+      tma_1d(cring_s + (uint32_t)(k % kRing) * kCBytes, (const uint8_t*)a.cidx + base * (cbytes / kTile), cbytes,
+             bar);
+    }
+  };
+  auto wait_seq = [&](uint64_t s) { mbar_wait(bar_s + 8 * (uint32_t)(s % kRing), (uint32_t)((s / kRing) & 1)); };
+
+  double acc0 = 0.0, acc0b = 0.0, acc1 = 0.0, acc1b = 0.0, acc2 = 0.0;
+  double2 v[NV][NR];
+
+  issue(0);
+  issue(1);
+  for (uint64_t k = 0; k < my_tiles; ++k) {
+    const uint64_t base = tile_base(a, blockIdx.x + k * gridDim.x);
+    const uint8_t* cs = cring + (uint32_t)(k % kRing) * kCBytes;
+    constexpr PhaseSpec P0 = shape_phase(SH, 0);
+    uint32_t lb = lbase<W>(P0, lane, warp);
+    uint32_t xs_addr;  // byte address of the exchange slot for this tile
+
+    if constexpr (NV == 1) {
+      issue(k + 2);
+      wait_seq(k);
+      xs_addr = ring_s + (uint32_t)(k % kRing) * kSlotBytes;
+      if (flags & SF_PLUS) {
+#pragma unroll
+        for (int j = 0; j < NR; ++j) v[0][j] = make_double2(a.plus_amp, 0.0);
+      } else {
+        const uint32_t p0 = xs_addr + lb * 16u;  // natural (TMA) layout
+#pragma unroll
+        for (int j = 0; j < NR; ++j) v[0][j] = lds(p0 + (((uint32_t)j << P0.reg_l) * 16u));
+      }
+    } else {
+      issue(2 * k + 2);  // bra of the next tile into the slot freed at the end of tile k-1
+      wait_seq(2 * k);
+      wait_seq(2 * k + 1);
+      const uint32_t b_addr = ring_s + (uint32_t)((2 * k) % kRing) * kSlotBytes;
+      xs_addr = ring_s + (uint32_t)((2 * k + 1) % kRing) * kSlotBytes;
+      if (!(flags & SF_BRA_FROM_KET)) {
+        const uint32_t p0 = b_addr + lb * 16u;
+#pragma unroll
+        for (int j = 0; j < NR; ++j) v[1][j] = lds(p0 + (((uint32_t)j << P0.reg_l) * 16u));
+      }
+      fence_proxy_async();
+      __syncthreads();
+      issue(2 * k + 3);  // ket of the next tile into the bra slot just read
+      const uint32_t p0 = xs_addr + lb * 16u;
+#pragma unroll
+      for (int j = 0; j < NR; ++j) v[0][j] = lds(p0 + (((uint32_t)j << P0.reg_l) * 16u));
+    }
+
+    // ---------------------------------------------------------------- pre ops
+    if (flags & (SF_PRE_PHASE | SF_BRA_FROM_KET | SF_PRE_DINNER)) {
+      const uint64_t g0 = base + gofs<IS_A>(lb, glo);
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        const uint32_t l = lb | ((uint32_t)j << P0.reg_l);
+        const uint64_t g = g0 + gofs<IS_A>((uint32_t)j << P0.reg_l, glo);
+        double t = 0.0;
+        if (flags & (SF_BRA_FROM_KET | SF_PRE_DINNER)) {
+          if constexpr (KSIN || !IS_A) t = a.table[g];
+          else t = a.vmin + (double)(a.kind == 1 ? cs[l] : ((const uint16_t*)cs)[l]);
+        }
+        if constexpr (NV == 2) {
+          if (flags & SF_BRA_FROM_KET) v[1][j] = make_double2(t * v[0][j].x, t * v[0][j].y);
+          if (flags & SF_PRE_DINNER) {
+            const double d = v[1][j].x * v[0][j].y - v[1][j].y * v[0][j].x;
+            if (j & 1) acc1b = fma(t, d, acc1b);
+            else acc1 = fma(t, d, acc1);
+          }
+        }
+        if (flags & SF_PRE_PHASE) {
+          double2 f;
+          if constexpr (KSIN || !IS_A) {
+            double sn, cn;
+            sincos(a.pre_ang * a.table[g], &sn, &cn);
+            f = make_double2(cn, sn);
+            if constexpr (!EXACT) f = cmul_fast(f, a.pre_extra);
+          } else {
+            f = a.kind == 1 ? slut[cs[l]] : __ldg(&a.lut[((const uint16_t*)cs)[l]]);
+          }
+#pragma unroll
+          for (int q = 0; q < NV; ++q) v[q][j] = cmul<EXACT>(v[q][j], f);
+        }
+      }
+    }
+
+    // ---------------------------------------------------------------- phases
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const PhaseSpec P = shape_phase(SH, p);
+      if (p > 0) {
+        // exchange through this tile's slot (swizzled), one vector at a time
+        const PhaseSpec Q = shape_phase(SH, p - 1);
+        const uint32_t nlb = lbase<W>(P, lane, warp);
+        const uint32_t so = swz(lb) * 16u, sn = swz(nlb) * 16u;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          __syncthreads();
+#pragma unroll
+          for (int j = 0; j < NR; ++j) sts(xs_addr + (so ^ (swz((uint32_t)j << Q.reg_l) * 16u)), v[q][j]);
+          __syncthreads();
+#pragma unroll
+          for (int j = 0; j < NR; ++j) v[q][j] = lds(xs_addr + (sn ^ (swz((uint32_t)j << P.reg_l) * 16u)));
+        }
+        lb = nlb;
+      }
+      const uint32_t apply = a.ph[p].apply;
+      if constexpr (NV == 2) {
+        // sum_j <bra|X_j|ket> for this phase's qubits, before any of its gates
+        // (X_j commutes with every Rx): one scale factor xs_w[p] covers them
+        if (flags & SF_XSUM) {
+          double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
+#pragma unroll
+          for (int b = 0; b < R; ++b) {
+            if (apply & (1u << b)) {
+#pragma unroll
+              for (int j = 0; j < NR; ++j) {
+                if (j & (1 << b)) continue;
+                const int k2 = j | (1 << b);
+                x0 = fma(v[1][j].x, v[0][k2].y, x0);
+                x1 = fma(-v[1][j].y, v[0][k2].x, x1);
+                x2 = fma(v[1][k2].x, v[0][j].y, x2);
+                x3 = fma(-v[1][k2].y, v[0][j].x, x3);
+              }
+            }
+          }
+          acc2 = fma(a.xs_w[p], (x0 + x1) + (x2 + x3), acc2);
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < R; ++b) {
+        if (apply & (1u << b)) {
+#pragma unroll
+          for (int j = 0; j < NR; ++j) {
+            if (j & (1 << b)) continue;
+            const int k2 = j | (1 << b);
+#pragma unroll
+            for (int q = 0; q < NV; ++q) butterfly<FORM>(v[q][j], v[q][k2], a.ga, a.gb);
+          }
+        }
+      }
+    }
+
+    // ---------------------------------------------------------------- post
+    constexpr int RL = shape_phase(SH, NP - 1).reg_l;
+    if constexpr (!EXACT) {
+      if (flags & SF_POST_SCALE) {
+        const double sc = a.post_scale;
+#pragma unroll
+        for (int q = 0; q < NV; ++q)
+#pragma unroll
+          for (int j = 0; j < NR; ++j) v[q][j] = make_double2(v[q][j].x * sc, v[q][j].y * sc);
+      }
+    }
+    const uint64_t g1 = base + gofs<IS_A>(lb, glo);
+    if (flags & (SF_POST_EXPECT | SF_POST_DINNER)) {
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        double t;
+        if (cidx_tma) {
+          const uint32_t l = lb | ((uint32_t)j << RL);
+          t = a.vmin + (double)(a.kind == 1 ? cs[l] : ((const uint16_t*)cs)[l]);
+        } else {
+          const uint64_t g = g1 + gofs<IS_A>((uint32_t)j << RL, glo);
+          t = a.kind == 0 ? a.table[g]
+                          : a.vmin + (double)(a.kind == 1 ? ((const uint8_t*)a.cidx)[g] : ((const uint16_t*)a.cidx)[g]);
+        }
+        double d;
+        if constexpr (NV == 1) d = fma(v[0][j].x, v[0][j].x, v[0][j].y * v[0][j].y);
+        else d = v[1][j].x * v[0][j].y - v[1][j].y * v[0][j].x;  // slot 0: PRE_DINNER may use slot 1
+        if (j & 1) acc0b = fma(t, d, acc0b);
+        else acc0 = fma(t, d, acc0);
+      }
+    }
+    if (!(flags & SF_NO_STORE)) {
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        double2* dst = (q == 0 ? a.v0 : a.v1) + g1;
+#pragma unroll
+        for (int j = 0; j < NR; ++j) st_stream(dst + gofs<IS_A>((uint32_t)j << RL, glo), v[q][j]);
+      }
+    }
+    fence_proxy_async();  // our generic-proxy smem writes before TMA refills the slot
+    __syncthreads();      // this tile's slots may be refilled from the next iteration on
+  }
+
+  // ------------------------------------------------------------ partial sums
+  if (a.partials) {
+    double* red = (double*)smem_raw;
+    acc0 = warp_sum(acc0 + acc0b);
+    acc1 = warp_sum(acc1 + acc1b);
+    acc2 = warp_sum(acc2);
+    constexpr int NW = 1 << W;
+    if (lane == 0) {
+      red[warp] = acc0;
+      red[NW + warp] = acc1;
+      red[2 * NW + warp] = acc2;
+    }
+    __syncthreads();
+    if (threadIdx.x < kSlots) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += red[threadIdx.x * NW + w];
+      a.partials[threadIdx.x * gridDim.x + blockIdx.x] = s;
+    }
+  }
+}
+
+template <int SH, int NV, int FORM, bool KSIN>
+struct SweepKernel {
+  static constexpr int threads = 32 << shape_w(SH);
+  static int grid(qsb_ctx* ctx, uint64_t ntiles, unsigned* g) {
+    static int occ = -1;  // per process; one device type
+    if (occ < 0) {
+      QSB_CUDA(cudaFuncSetAttribute(k_sweep<SH, NV, FORM, KSIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kSmemBytes));
+      int o = 0;
+      QSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sweep<SH, NV, FORM, KSIN>, threads, kSmemBytes));
+      occ = o < 1 ? 1 : o;
+    }
+    const uint64_t want = (uint64_t)ctx->num_sms * occ;
+    *g = (unsigned)(ntiles < want ? ntiles : want);
+    return QSB_OK;
+  }
+  static int launch(qsb_ctx* ctx, SweepArgs& a, unsigned* gout) {
+    unsigned g;
+    QSB_TRY(grid(ctx, a.ntiles, &g));
+    k_sweep<SH, NV, FORM, KSIN><<<g, threads, kSmemBytes, ctx->stream>>>(a);
+    QSB_CHECK_LAUNCH(ctx, "sweep");
+    if (gout) *gout = g;
+    return QSB_OK;
+  }
+};
+
+// pick the instantiation for (shape, form, table kind) and call f(kernel-type)
+template <int NV, int SA, int SAX, int SB, class F>
+int dispatch_nv(const SweepArgs& a, F&& f) {
+  const bool ksin = a.kind == 0;
+  if (a.shape == SAX) return ksin ? f(SweepKernel<SAX, NV, GF_EXACT, true>{}) : f(SweepKernel<SAX, NV, GF_EXACT, false>{});
+  if (a.shape == SA) {
+    if (a.form == GF_FACT_C) return ksin ? f(SweepKernel<SA, NV, GF_FACT_C, true>{}) : f(SweepKernel<SA, NV, GF_FACT_C, false>{});
+    if (a.form == GF_FACT_S) return ksin ? f(SweepKernel<SA, NV, GF_FACT_S, true>{}) : f(SweepKernel<SA, NV, GF_FACT_S, false>{});
+    return invalid("internal: exact gates need the exact A shape");
+  }
+  if (a.form == GF_FACT_C) return f(SweepKernel<SB, NV, GF_FACT_C, false>{});
+  if (a.form == GF_FACT_S) return f(SweepKernel<SB, NV, GF_FACT_S, false>{});
+  return f(SweepKernel<SB, NV, GF_EXACT, false>{});
+}
+
+}  // namespace sweepk
+}  // namespace qsb

@@ -206,12 +206,9 @@ int qsb_table_wrap(qsb_ctx* ctx, int n, double* values, double* min_out, double*
   return QSB_OK;
 }
 
+// Does not touch t->ctx (it may already be destroyed); cudaFree synchronises.
 int qsb_table_destroy(qsb_table* t) {
   if (!t) return QSB_OK;
-  if (t->ctx) {
-    cudaSetDevice(t->ctx->device);
-    cudaStreamSynchronize(t->ctx->stream);
-  }
   if (t->cidx) cudaFree(t->cidx);
   if (t->d_lut) cudaFree(t->d_lut);
   delete t;
