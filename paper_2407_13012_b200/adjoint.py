@@ -41,7 +41,7 @@ def _walk(handle: circuit.SimHandle, params: circuit.QaoaParams, want_value: boo
     p = params.p
     if p < 1:
         raise ContractViolation("gradient needs depth p >= 1")
-    bra = backend.alloc_state_uninitialized(handle.n, handle.ctx)
+    bra = handle._adjoint_state()
     try:
         value, dg, db = handle.ctx.kernels.value_and_grad(
             handle.state.data, bra.data, handle.table.values.data, handle.n, params.gammas, params.betas,

@@ -2,6 +2,7 @@
 // expectation, value_and_grad (adjoint walk over exactly two vectors) and the
 // Rx layer.  Reference: circuit.py:98-113, adjoint.py:37-77, backend.py:200-207.
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -45,18 +46,31 @@ std::vector<SweepShape> plan_sweeps(int n) {
   return out;
 }
 
+// register-bit family of the fast sweeps (QSB_SWEEP_R1 / QSB_SWEEP_R2 override)
+int sweep_family(int nv) {
+  static int fam[3] = {0, 0, 0};
+  if (!fam[nv]) {
+    const char* e = getenv(nv == 1 ? "QSB_SWEEP_R1" : "QSB_SWEEP_R2");
+    int r = e ? atoi(e) : 0;
+    if (nv == 2 && r == 5) r = 0;  // two vectors of 32 amplitudes do not fit in registers
+    if (r < 3 || r > 5) r = 4;  // measured best for both kinds on B200 (profiles/)
+    fam[nv] = r;
+  }
+  return fam[nv];
+}
+
 // Fill the tile/phase part of SweepArgs for one sweep. Returns the number of gates.
 int build_shape(const SweepShape& sh, int n, int nv, bool exact, SweepArgs& a, int gates_before_phase[kMaxPhases]) {
   int gl[kSweepT];
   for (int i = 0; i < kSweepT; ++i) gl[i] = sh.is_a ? i : (i < 3 ? i : sh.glo + i - 3);
-  const int shape = pick_shape(nv, exact, sh.is_a);
+  const int shape = pick_shape(exact, sh.is_a, sweep_family(nv));
   const int np = shape_np(shape);
   PhaseSpec ps[kMaxPhases];
   for (int p = 0; p < np; ++p) ps[p] = shape_phase(shape, p);
   a.shape = shape;
   a.glo = sh.is_a ? 3 : sh.glo;
-  const int R = nv == 1 ? 5 : 4;
-  const int W = nv == 1 ? 2 : 3;
+  const int R = shape_r(shape);
+  const int W = shape_w(shape);
   bool applied[kSweepT] = {false};
   int gates = 0;
   a.nphase = np;
@@ -280,11 +294,14 @@ struct Runner {
     if (gates < 0) return invalid("internal: bad sweep layout");
     a.v0 = v0;
     a.v1 = v1;
+    set_table(a, t);
+    const bool table_ops = flags & (SF_PRE_PHASE | SF_BRA_FROM_KET | SF_PRE_DINNER | SF_POST_EXPECT | SF_POST_DINNER);
+    a.cmode = (t && t->kind != 0 && table_ops) ? ((!sh.is_a && t->kind == 1) ? 2 : 1) : 0;
     if (!sh.is_a) {  // TMA boxes for the strided B tiles
       QSB_TRY(encode_b_tile_map(&a.tm0, v0, n, sh.glo));
       if (nv == 2) QSB_TRY(encode_b_tile_map(&a.tm1, v1, n, sh.glo));
+      if (a.cmode) QSB_TRY(encode_b_cidx_map(&a.tmc, t->cidx, t->kind == 1 ? 1 : 2, n, sh.glo));
     }
-    set_table(a, t);
     a.lut = lut;
     a.pre_ang = pre_ang;
     a.pre_extra = pre_extra;

@@ -1,4 +1,4 @@
-// Fused multi-qubit sweep: descriptor shared by the kernel (sweep.cu) and the
+// Fused multi-qubit sweep: descriptor shared by the kernel (sweep_impl.cuh) and the
 // host-side planner / orchestration (fused.cu).
 #pragma once
 #include <cuda.h>  // CUtensorMap (TMA descriptors; encoded through the runtime driver entry point)
@@ -40,6 +40,7 @@ struct PhaseMap {
 
 struct SweepArgs {
   CUtensorMap tm0, tm1;   // B shapes: 5-D TMA boxes over v0 / v1 (one 64 KB tile per load)
+  CUtensorMap tmc;        // B shapes with table ops: 5-D box over the compact index (cmode)
   double2* v0;            // ket / the single vector
   double2* v1;            // bra (NV=2)
   const void* cidx;       // compact table index (kind 1: u8, 2: u16)
@@ -63,6 +64,7 @@ struct SweepArgs {
   uint8_t run_pos[4], run_len[4];
   int cshift;             // global bit of local bit 3 (cidx 8-entry chunk c -> base + (c << cshift))
   int shape;              // SweepShapeId
+  int cmode;              // compact index tile in smem: 0 none, 1 natural order, 2 B-tile u8 (16-wide rows)
   int glo;                // B shapes: global bit of local bit 3
   PhaseMap ld;            // cp.async load mapping: lanes <-> local 0..4 (coalesced)
   PhaseMap ph[kMaxPhases];
@@ -82,14 +84,18 @@ struct PhaseSpec {
   bool allow;
 };
 
-enum SweepShapeId : int { SH_A1 = 0, SH_A1X = 1, SH_B1 = 2, SH_A2 = 3, SH_A2X = 4, SH_B2 = 5 };
+// Families: R=5 (4 warps, shapes 0-2), R=4 (8 warps, 3-5), R=3 (16 warps, 6-7).
+enum SweepShapeId : int {
+  SH_A1 = 0, SH_A1X = 1, SH_B1 = 2, SH_A2 = 3, SH_A2X = 4, SH_B2 = 5, SH_A3 = 6, SH_B3 = 7
+};
 
 __host__ __device__ constexpr int shape_np(int sh) {
-  return sh == SH_A1 ? 3 : sh == SH_A1X ? 4 : sh == SH_B1 ? 2 : sh == SH_A2 ? 3 : sh == SH_A2X ? 4 : 3;
+  return sh == SH_A1 ? 3 : sh == SH_A1X ? 4 : sh == SH_B1 ? 2 : sh == SH_A2 ? 3 : sh == SH_A2X ? 4
+       : sh == SH_B2 ? 3 : sh == SH_A3 ? 4 : 3;
 }
-__host__ __device__ constexpr bool shape_is_a(int sh) { return sh != SH_B1 && sh != SH_B2; }
-__host__ __device__ constexpr int shape_r(int sh) { return sh <= SH_B1 ? 5 : 4; }
-__host__ __device__ constexpr int shape_w(int sh) { return sh <= SH_B1 ? 2 : 3; }
+__host__ __device__ constexpr bool shape_is_a(int sh) { return sh != SH_B1 && sh != SH_B2 && sh != SH_B3; }
+__host__ __device__ constexpr int shape_r(int sh) { return sh <= SH_B1 ? 5 : sh <= SH_B2 ? 4 : 3; }
+__host__ __device__ constexpr int shape_w(int sh) { return sh <= SH_B1 ? 2 : sh <= SH_B2 ? 3 : 4; }
 
 __host__ __device__ constexpr PhaseSpec shape_phase(int sh, int p) {
   // clang-format off
@@ -109,14 +115,24 @@ __host__ __device__ constexpr PhaseSpec shape_phase(int sh, int p) {
                       : p == 1 ? PhaseSpec{{4, 5, 6, 7, 8}, {9, 10, 11, 0}, 0, true}
                       : p == 2 ? PhaseSpec{{0, 1, 2, 3, 8}, {9, 10, 11, 0}, 4, true}
                       :          PhaseSpec{{0, 1, 2, 3, 4}, {5, 6, 7, 0}, 8, true})
-       :                (p == 0 ? PhaseSpec{{0, 1, 2, 7, 8}, {9, 10, 11, 0}, 3, true}
+       : sh == SH_B2 ? (p == 0 ? PhaseSpec{{0, 1, 2, 7, 8}, {9, 10, 11, 0}, 3, true}
                       : p == 1 ? PhaseSpec{{0, 1, 2, 3, 4}, {9, 10, 11, 0}, 5, true}
-                      :          PhaseSpec{{0, 1, 2, 3, 4}, {5, 6, 7, 0}, 8, true});
+                      :          PhaseSpec{{0, 1, 2, 3, 4}, {5, 6, 7, 0}, 8, true})
+       : sh == SH_A3 ? (p == 0 ? PhaseSpec{{0, 1, 2, 3, 4}, {5, 6, 7, 8}, 9, true}
+                      : p == 1 ? PhaseSpec{{3, 4, 5, 6, 7}, {8, 9, 10, 11}, 0, true}
+                      : p == 2 ? PhaseSpec{{0, 1, 2, 6, 7}, {8, 9, 10, 11}, 3, true}
+                      :          PhaseSpec{{0, 1, 2, 3, 4}, {5, 9, 10, 11}, 6, true})
+       :                (p == 0 ? PhaseSpec{{0, 1, 2, 6, 7}, {8, 9, 10, 11}, 3, true}
+                      : p == 1 ? PhaseSpec{{0, 1, 2, 3, 4}, {5, 9, 10, 11}, 6, true}
+                      :          PhaseSpec{{0, 1, 2, 3, 4}, {5, 6, 7, 8}, 9, true});
   // clang-format on
 }
 
-__host__ __device__ constexpr int pick_shape(int nv, bool exact, bool is_a) {
-  return nv == 1 ? (is_a ? (exact ? SH_A1X : SH_A1) : SH_B1) : (is_a ? (exact ? SH_A2X : SH_A2) : SH_B2);
+// family r in {5, 4, 3} for fast mode; exact mode always uses the R=4 shapes
+// (ascending qubit order: A2X, B2)
+__host__ __device__ constexpr int pick_shape(bool exact, bool is_a, int r) {
+  return exact ? (is_a ? SH_A2X : SH_B2)
+       : r == 5 ? (is_a ? SH_A1 : SH_B1) : r == 4 ? (is_a ? SH_A2 : SH_B2) : (is_a ? SH_A3 : SH_B3);
 }
 
 // launch one sweep (picks the instantiation from a.shape / a.form / a.kind);
@@ -124,6 +140,8 @@ __host__ __device__ constexpr int pick_shape(int nv, bool exact, bool is_a) {
 int launch_sweep(qsb_ctx* ctx, int nv, bool exact, SweepArgs& a, unsigned* grid_out);
 // 5-D box over a statevector for a B-shape tile with local bit 3 at global bit glo
 int encode_b_tile_map(CUtensorMap* map, const double2* base, int n, int glo);
+// 5-D box over the compact index (esz 1 or 2 bytes) for the same B tile
+int encode_b_cidx_map(CUtensorMap* map, const void* base, int esz, int n, int glo);
 int sweep_grid(qsb_ctx* ctx, int nv, bool exact, uint64_t ntiles, unsigned* grid_out);
 
 }  // namespace qsb

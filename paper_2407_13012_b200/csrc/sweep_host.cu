@@ -5,24 +5,29 @@
 
 namespace qsb {
 
-int launch_sweep_nv1(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
-int launch_sweep_nv2(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
-int grid_sweep_nv1(qsb_ctx* ctx, SweepArgs& a, uint64_t ntiles, unsigned* g);
-int grid_sweep_nv2(qsb_ctx* ctx, SweepArgs& a, uint64_t ntiles, unsigned* g);
+int launch_sweep_nv1_r5(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int launch_sweep_nv1_r4(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int launch_sweep_nv1_r3(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int launch_sweep_nv2_r4(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int launch_sweep_nv2_r3(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int launch_sweep_exact_nv1(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int launch_sweep_exact_nv2(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 
 int launch_sweep(qsb_ctx* ctx, int nv, bool exact, SweepArgs& a, unsigned* gout) {
-  (void)exact;  // a.shape / a.form carry the choice
-  return nv == 1 ? launch_sweep_nv1(ctx, a, gout) : launch_sweep_nv2(ctx, a, gout);
+  if (exact || a.form == GF_EXACT) return nv == 1 ? launch_sweep_exact_nv1(ctx, a, gout) : launch_sweep_exact_nv2(ctx, a, gout);
+  const int r = shape_r(a.shape);
+  if (nv == 1) return r == 5 ? launch_sweep_nv1_r5(ctx, a, gout) : r == 4 ? launch_sweep_nv1_r4(ctx, a, gout)
+                                                                           : launch_sweep_nv1_r3(ctx, a, gout);
+  if (r == 5) return invalid("internal: no R=5 bra/ket sweep");
+  return r == 4 ? launch_sweep_nv2_r4(ctx, a, gout) : launch_sweep_nv2_r3(ctx, a, gout);
 }
 
 int sweep_grid(qsb_ctx* ctx, int nv, bool exact, uint64_t ntiles, unsigned* g) {
-  // all shapes run one persistent CTA per SM; query the A-shape instantiation
-  SweepArgs a;
-  memset(&a, 0, sizeof(a));
-  a.shape = pick_shape(nv, exact, true);
-  a.form = exact ? GF_EXACT : GF_FACT_C;
-  a.kind = 1;
-  return nv == 1 ? grid_sweep_nv1(ctx, a, ntiles, g) : grid_sweep_nv2(ctx, a, ntiles, g);
+  // every shape runs one persistent CTA per SM (the ring takes ~220 KB of smem)
+  (void)nv;
+  (void)exact;
+  *g = (unsigned)(ntiles < (uint64_t)ctx->num_sms ? ntiles : (uint64_t)ctx->num_sms);
+  return QSB_OK;
 }
 
 namespace {
@@ -61,6 +66,33 @@ int encode_b_tile_map(CUtensorMap* map, const double2* base, int n, int glo) {
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return invalid("cuTensorMapEncodeTiled failed (%d) for n=%d glo=%d", (int)r, n, glo);
+  return QSB_OK;
+}
+
+// Compact index of the same B tile.  u16: inner 8 entries (16 B) = local bits 0..2,
+// natural local order in smem.  u8: the inner box must be 16 B, so it covers global
+// bits 0..3 — bit 3 is the lowest tile-index bit (glo >= 4 for every B sweep); the
+// tile's 8 entries sit at ((l >> 3) << 4) + 8 * (tile & 1) + (l & 7) in smem.
+int encode_b_cidx_map(CUtensorMap* map, const void* base, int esz, int n, int glo) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return invalid("cuTensorMapEncodeTiled unavailable (driver too old?)");
+  if (glo < 4 || n - glo - 9 < 0) return invalid("internal: bad B index geometry n=%d glo=%d", n, glo);
+  CUresult r;
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  if (esz == 2) {
+    const cuuint64_t dims[5] = {8, 1ull << (glo - 3), 32, 16, 1ull << (n - glo - 9)};
+    const cuuint64_t strides[4] = {16, (1ull << glo) * 2, (1ull << (glo + 5)) * 2, (1ull << (glo + 9)) * 2};
+    const cuuint32_t box[5] = {8, 1, 32, 16, 1};
+    r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 5, (void*)base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    const cuuint64_t dims[5] = {16, 1ull << (glo - 4), 32, 16, 1ull << (n - glo - 9)};
+    const cuuint64_t strides[4] = {16, 1ull << glo, 1ull << (glo + 5), 1ull << (glo + 9)};
+    const cuuint32_t box[5] = {16, 1, 32, 16, 1};
+    r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, (void*)base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (r != CUDA_SUCCESS) return invalid("cuTensorMapEncodeTiled (index) failed (%d) n=%d glo=%d", (int)r, n, glo);
   return QSB_OK;
 }
 

@@ -162,17 +162,16 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t flags = a.flags;
   const int glo = a.glo;
-  // compact-index tiles ride the A-tile TMA (B shapes read the table from HBM)
-  const bool cidx_tma = IS_A && !KSIN && a.kind != 0 &&
-                        (flags & (SF_PRE_PHASE | SF_BRA_FROM_KET | SF_PRE_DINNER | SF_POST_EXPECT | SF_POST_DINNER));
-  const uint32_t cbytes = a.kind == 2 ? 2u * kTile : kTile;
+  // compact-index tiles ride the TMA of the tile's first vector (cmode, see sweep.cuh)
+  const int cmode = KSIN ? 0 : a.cmode;
+  const uint32_t cbytes = IS_A ? (a.kind == 2 ? 2u * kTile : kTile) : 2u * kTile;
 
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int s = 0; s < kRing; ++s) mbar_init(bar_s + 8 * s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (!KSIN && a.kind == 1 && (flags & SF_PRE_PHASE)) {
+  if (!KSIN && a.kind == 1 && (flags & SF_PRE_PHASE)) {  // u8 LUT in smem
     for (int i = threadIdx.x; i < a.nlut; i += NT) slut[i] = a.lut[i];
   }
   __syncthreads();
@@ -190,7 +189,7 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
     const uint32_t slot = (uint32_t)(s % kRing);
     const uint32_t bar = bar_s + 8 * slot;
     const bool vec = !((q == 0 && (flags & SF_PLUS)) || (q == 1 && (flags & SF_BRA_FROM_KET)));
-    const bool cid = cidx_tma && (s % NV) == 0;
+    const bool cid = cmode != 0 && (s % NV) == 0;
     const uint32_t bytes = (vec ? kSlotBytes : 0u) + (cid ? cbytes : 0u);
     if (bytes == 0) {
       mbar_arrive(bar);
@@ -209,9 +208,14 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
       }
     }
     if (cid) {
-      const uint64_t base = tile << kSweepT;
-      tma_1d(cring_s + (uint32_t)(k % kRing) * kCBytes, (const uint8_t*)a.cidx + base * (cbytes / kTile), cbytes,
-             bar);
+      const uint32_t cdst = cring_s + (uint32_t)(k % kRing) * kCBytes;
+      if constexpr (IS_A) {
+        tma_1d(cdst, (const uint8_t*)a.cidx + (tile << kSweepT) * (cbytes / kTile), cbytes, bar);
+      } else {
+        const int lowbits = glo - 3;
+        const int c1 = (int)(tile & ((1ull << lowbits) - 1ull));
+        tma_5d(cdst, &a.tmc, cmode == 2 ? (c1 >> 1) : c1, (int)(tile >> lowbits), bar);
+      }
     }
   };
   auto wait_seq = [&](uint64_t s) { mbar_wait(bar_s + 8 * (uint32_t)(s % kRing), (uint32_t)((s / kRing) & 1)); };
@@ -219,11 +223,19 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
   double acc0 = 0.0, acc0b = 0.0, acc1 = 0.0, acc1b = 0.0, acc2 = 0.0;
   double2 v[NV][NR];
 
+  // cost value of local index l (global index g): compact index tile in smem, or the f64 table
+  auto cval = [&](const uint8_t* cs, uint32_t tb8, uint32_t l, uint64_t g) -> double {
+    if (cmode == 0) return a.table[g];
+    if (cmode == 2) return a.vmin + (double)cs[((l >> 3) << 4) | tb8 | (l & 7u)];
+    return a.vmin + (double)(a.kind == 1 ? cs[l] : ((const uint16_t*)cs)[l]);
+  };
+
   issue(0);
   issue(1);
   for (uint64_t k = 0; k < my_tiles; ++k) {
     const uint64_t base = tile_base(a, blockIdx.x + k * gridDim.x);
     const uint8_t* cs = cring + (uint32_t)(k % kRing) * kCBytes;
+    const uint32_t tb8 = (uint32_t)((blockIdx.x + k * gridDim.x) & 1u) << 3;  // cmode 2: tile's half of each row
     constexpr PhaseSpec P0 = shape_phase(SH, 0);
     uint32_t lb = lbase<W>(P0, lane, warp);
     uint32_t xs_addr;  // byte address of the exchange slot for this tile
@@ -267,10 +279,7 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
         const uint32_t l = lb | ((uint32_t)j << P0.reg_l);
         const uint64_t g = g0 + gofs<IS_A>((uint32_t)j << P0.reg_l, glo);
         double t = 0.0;
-        if (flags & (SF_BRA_FROM_KET | SF_PRE_DINNER)) {
-          if constexpr (KSIN || !IS_A) t = a.table[g];
-          else t = a.vmin + (double)(a.kind == 1 ? cs[l] : ((const uint16_t*)cs)[l]);
-        }
+        if (flags & (SF_BRA_FROM_KET | SF_PRE_DINNER)) t = cval(cs, tb8, l, g);
         if constexpr (NV == 2) {
           if (flags & SF_BRA_FROM_KET) v[1][j] = make_double2(t * v[0][j].x, t * v[0][j].y);
           if (flags & SF_PRE_DINNER) {
@@ -281,11 +290,13 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
         }
         if (flags & SF_PRE_PHASE) {
           double2 f;
-          if constexpr (KSIN || !IS_A) {
+          if constexpr (KSIN) {
             double sn, cn;
             sincos(a.pre_ang * a.table[g], &sn, &cn);
             f = make_double2(cn, sn);
             if constexpr (!EXACT) f = cmul_fast(f, a.pre_extra);
+          } else if (cmode == 2) {
+            f = slut[cs[((l >> 3) << 4) | tb8 | (l & 7u)]];
           } else {
             f = a.kind == 1 ? slut[cs[l]] : __ldg(&a.lut[((const uint16_t*)cs)[l]]);
           }
@@ -367,15 +378,7 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
     if (flags & (SF_POST_EXPECT | SF_POST_DINNER)) {
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
-        double t;
-        if (cidx_tma) {
-          const uint32_t l = lb | ((uint32_t)j << RL);
-          t = a.vmin + (double)(a.kind == 1 ? cs[l] : ((const uint16_t*)cs)[l]);
-        } else {
-          const uint64_t g = g1 + gofs<IS_A>((uint32_t)j << RL, glo);
-          t = a.kind == 0 ? a.table[g]
-                          : a.vmin + (double)(a.kind == 1 ? ((const uint8_t*)a.cidx)[g] : ((const uint16_t*)a.cidx)[g]);
-        }
+        const double t = cval(cs, tb8, lb | ((uint32_t)j << RL), g1 + gofs<IS_A>((uint32_t)j << RL, glo));
         double d;
         if constexpr (NV == 1) d = fma(v[0][j].x, v[0][j].x, v[0][j].y * v[0][j].y);
         else d = v[1][j].x * v[0][j].y - v[1][j].y * v[0][j].x;  // slot 0: PRE_DINNER may use slot 1
@@ -443,19 +446,26 @@ struct SweepKernel {
   }
 };
 
-// pick the instantiation for (shape, form, table kind) and call f(kernel-type)
-template <int NV, int SA, int SAX, int SB, class F>
-int dispatch_nv(const SweepArgs& a, F&& f) {
+// fast-mode instantiations of one register family (A shape SA, B shape SB)
+template <int NV, int SA, int SB>
+int launch_fast(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
+  auto L = [&](auto k) { return decltype(k)::launch(ctx, a, g); };
   const bool ksin = a.kind == 0;
-  if (a.shape == SAX) return ksin ? f(SweepKernel<SAX, NV, GF_EXACT, true>{}) : f(SweepKernel<SAX, NV, GF_EXACT, false>{});
+  const bool c = a.form == GF_FACT_C;
   if (a.shape == SA) {
-    if (a.form == GF_FACT_C) return ksin ? f(SweepKernel<SA, NV, GF_FACT_C, true>{}) : f(SweepKernel<SA, NV, GF_FACT_C, false>{});
-    if (a.form == GF_FACT_S) return ksin ? f(SweepKernel<SA, NV, GF_FACT_S, true>{}) : f(SweepKernel<SA, NV, GF_FACT_S, false>{});
-    return invalid("internal: exact gates need the exact A shape");
+    if (c) return ksin ? L(SweepKernel<SA, NV, GF_FACT_C, true>{}) : L(SweepKernel<SA, NV, GF_FACT_C, false>{});
+    return ksin ? L(SweepKernel<SA, NV, GF_FACT_S, true>{}) : L(SweepKernel<SA, NV, GF_FACT_S, false>{});
   }
-  if (a.form == GF_FACT_C) return f(SweepKernel<SB, NV, GF_FACT_C, false>{});
-  if (a.form == GF_FACT_S) return f(SweepKernel<SB, NV, GF_FACT_S, false>{});
-  return f(SweepKernel<SB, NV, GF_EXACT, false>{});
+  return c ? L(SweepKernel<SB, NV, GF_FACT_C, false>{}) : L(SweepKernel<SB, NV, GF_FACT_S, false>{});
+}
+
+// exact-mode instantiations (ascending qubit order, FMA-free): shapes A2X / B2
+template <int NV>
+int launch_exact(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
+  auto L = [&](auto k) { return decltype(k)::launch(ctx, a, g); };
+  if (a.shape == SH_A2X)
+    return a.kind == 0 ? L(SweepKernel<SH_A2X, NV, GF_EXACT, true>{}) : L(SweepKernel<SH_A2X, NV, GF_EXACT, false>{});
+  return L(SweepKernel<SH_B2, NV, GF_EXACT, false>{});
 }
 
 }  // namespace sweepk

@@ -1,0 +1,8 @@
+// Fast-mode sweep instantiations: NV=2, shapes SH_A3 / SH_B3 (see sweep_impl.cuh).
+#include "sweep_impl.cuh"
+
+namespace qsb {
+int launch_sweep_nv2_r3(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
+  return sweepk::launch_fast<2, SH_A3, SH_B3>(ctx, a, g);
+}
+}  // namespace qsb
