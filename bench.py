@@ -7,8 +7,11 @@ A step is one `value_and_grad(handle, params)` through the public API: forward
 simulation from |+>, <C>, and the gradient over all 2p angles (bra/ket adjoint
 walk).  Inputs are resident in HBM (the cost table, built once per handle);
 the 16 GiB statevector exceeds the 126 MB L2 by >100x, so no L2 flush is needed.
-For N > 1 (torchrun) every rank runs an independent replica on its own GPU
-(weak scaling, no data-path collective); value = all ranks' steps / max time.
+For N > 1 (torchrun, one process per GPU) the statevector is sharded over the N
+GPUs (paper_2407_13012_b200/dist.py: top log2 N qubits global, NCCL all-to-all
+index-bit swaps); weak scaling keeps 2^30 amplitudes per GPU (n = 30 + log2 N)
+and value counts n=30-equivalent evaluations (steps * 2^(n-30) / max-over-ranks
+device time).  `--replicas` runs N independent n=30 replicas instead.
 
 `--impl reference` times the reference's CPU path on the host cores instead:
 the oracle port (oracle/qaoa_oracle.cpp, a restatement of the reference's numba
@@ -26,6 +29,8 @@ import subprocess
 import sys
 import time
 from pathlib import Path
+
+import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
@@ -45,6 +50,7 @@ def parse():
     ap.add_argument("--p", type=int, default=DEPTH)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--params", choices=["ramp", "random"], default="ramp")
+    ap.add_argument("--replicas", action="store_true", help="N > 1: independent n=30 replicas instead of sharding")
     return ap.parse_args()
 
 
@@ -52,7 +58,8 @@ def workload(n: int, p: int, kind: str):
     import paper_2407_13012_b200 as qs
     from paper_2407_13012_b200 import rng
 
-    poly = qs.maxcut_polynomial(qs.random_regular(n, 3, seed=1))
+    # 3-regular graphs need an even vertex count: odd n (sharded weak scaling) uses degree 4
+    poly = qs.maxcut_polynomial(qs.random_regular(n, 3 if n % 2 == 0 else 4, seed=1))
     if kind == "ramp":
         params = qs.linear_ramp_params(p)
     else:  # conftest.random_params(1, p): no beta = 0 layer
@@ -260,6 +267,83 @@ def load_traffic() -> dict:
     return json.loads(p.read_text()) if p.exists() else {}
 
 
+def run_sharded(args, rank: int, world: int, dist) -> None:
+    """N > 1: one n-qubit state sharded over all N GPUs (top log2 N qubits global),
+    index-bit swaps by NCCL all-to-all.  Weak scaling: n = 30 + log2 N keeps 2^30
+    amplitudes per GPU (unless --n is given)."""
+    import torch
+
+    import paper_2407_13012_b200 as qs
+    from paper_2407_13012_b200 import dist as qdist
+
+    g = world.bit_length() - 1
+    if 1 << g != world:
+        raise SystemExit("sharded bench needs a power-of-two GPU count")
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n = args.n if args.n != N_QUBITS else N_QUBITS + g
+    poly, params = workload(n, args.p, args.params)
+    ex = qdist.TorchExchanger(g, dist, local)
+    t0 = time.perf_counter()
+    sh = qdist.ShardedHandle(poly, g, ex, device=local)
+    torch.cuda.synchronize(local)
+    setup_s = time.perf_counter() - t0
+    dev = sh.ctx.device
+    for _ in range(args.warmup):
+        sh.value_and_grad(params)
+    dist.barrier()
+    dev.sync()
+    torch.cuda.synchronize(local)
+    launches0 = dev.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            value, dg, db = sh.value_and_grad(params)
+        dev.sync()
+        torch.cuda.synchronize(local)
+        ev1.record()
+        ev1.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = dev.launches() - launches0
+    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    if rank == 0:
+        work = 2.0 ** (n - N_QUBITS)  # n=30-equivalent evaluations per step
+        line = {
+            "metric": METRIC,
+            "value": args.steps * work / (ms / 1e3),
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "c128",
+            "data": "synthetic (reference graph generator, seed 1)",
+            "config": {
+                "workload": f"sharded MaxCut regular graph n={n} (random_regular(n,{3 if n % 2 == 0 else 4},seed=1)) "
+                            f"over {world} GPUs (top {g} qubits global, NCCL all-to-all index-bit swaps), p={args.p}; "
+                            f"one step = expectation + full adjoint gradient",
+                "n": n, "p": args.p, "global_batch": 1, "parallelism": f"statevector sharded x{world}",
+                "value_definition": f"steps * 2^(n-30) / time: n=30-equivalent E+grad evaluations/s",
+                "l2": "no flush: 16 GiB per-GPU shard >> 126 MB L2",
+            },
+            "expectation": value,
+            "grad_norm_inf": float(max(np.abs(dg).max(), np.abs(db).max())),
+            "setup_s": setup_s,
+            "gpu_launches": launches,
+            "e2e": {"value": args.steps * work / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 16 * args.p,
+                    "d2h_bytes_per_step": 0,
+                    "how": "host params in, host E/gradient out through dist.ShardedHandle (device-event timed)"},
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    sh.close()
+
+
 def run_b200(args, rank: int, world: int, dist) -> None:
     import numpy as np
 
@@ -406,7 +490,10 @@ def main():
         if args.impl == "reference":
             run_reference(args, rank, world)
         else:
-            run_b200(args, rank, world, dist)
+            if world > 1 and not args.replicas:
+                run_sharded(args, rank, world, dist)
+            else:
+                run_b200(args, rank, world, dist)
     finally:
         if dist is not None:
             dist.barrier()

@@ -40,6 +40,17 @@ extern "C" {
                              to the numba kernel set (numba_impl.py:47-72) */
 #define QSB_FROM_PLUS 2u  /* (simulate) start from |+>, the input state is not read */
 
+/* fused-op flags of qsb_layer_sweeps (the sweep kernel's SweepFlags) */
+#define QSB_SW_PLUS 1u           /* input is |+> (not read) */
+#define QSB_SW_PRE_PHASE 2u      /* multiply by exp(i * phase_scale * C) before the gates */
+#define QSB_SW_BRA_FROM_KET 4u   /* nv=2: bra = C * ket (bra not read) */
+#define QSB_SW_PRE_DINNER 8u     /* nv=2: sums[1] += Im <bra|C|ket> before the phase */
+#define QSB_SW_XSUM 16u          /* nv=2: sums[2] += Im sum_j <bra|X_j|ket> over the gated qubits */
+#define QSB_SW_POST_EXPECT 32u   /* nv=1: sums[0] += <psi|C|psi> after the gates */
+#define QSB_SW_POST_DINNER 64u   /* nv=2: sums[0] += Im <bra|C|ket> after the gates */
+#define QSB_SW_NO_STORE 128u     /* results are not written back */
+#define QSB_SW_EXACT 65536u      /* FMA-free, ascending-order arithmetic */
+
 typedef struct qsb_ctx qsb_ctx;
 typedef struct qsb_table qsb_table;
 
@@ -111,6 +122,11 @@ int qsb_pairwise_level(qsb_ctx* ctx, const double* src, double* dst, uint64_t ds
  * owned (the RealBuffer of CostTable.values). */
 int qsb_table_create(qsb_ctx* ctx, int n, const double* weights, const int64_t* masks, uint64_t num_terms,
                      double* values, double* min_out, double* max_out, qsb_table** out);
+/* shard of a 2^n_global table for a sharded statevector: local index i of `rank`
+ * evaluates x = (i & (2^b-1)) | (rank << s1) | ((i >> b) << s2) */
+int qsb_table_create_mapped(qsb_ctx* ctx, int n_global, int n_local, const double* weights, const int64_t* masks,
+                            uint64_t num_terms, int b, int s1, int s2, uint64_t rank, double* values,
+                            double* min_out, double* max_out, qsb_table** out);
 /* wrap an already-filled device table (e.g. uploaded by the user) */
 int qsb_table_wrap(qsb_ctx* ctx, int n, double* values, double* min_out, double* max_out, qsb_table** out);
 int qsb_table_destroy(qsb_table* t);
@@ -132,6 +148,10 @@ int qsb_simulate_expect(qsb_ctx* ctx, qsb_table* t, double* amps, int p, const d
                         const double* betas, unsigned flags, double* expect_out);
 /* Rx(theta) on every qubit of amps (backend.apply_rx_layer, backend.py:200-207) */
 int qsb_rx_layer(qsb_ctx* ctx, double* amps, int n, double theta, unsigned flags);
+/* Rx(theta) on qubits [lo, hi] with fused ops (QSB_SW_*); sums[3] = partial sums
+ * (see fused.cu).  Building block of the sharded walk. */
+int qsb_layer_sweeps(qsb_ctx* ctx, qsb_table* t, double* v0, double* v1, int nv, int n, int lo, int hi,
+                     double theta, unsigned flags, double phase_scale, double* sums);
 /* <psi|C|psi> (circuit.expectation_of_state, circuit.py:106-113, without the clamp) */
 int qsb_expectation(qsb_ctx* ctx, qsb_table* t, const double* amps, unsigned flags, double* out);
 /* expectation + adjoint gradient (adjoint.py:37-77): one forward, one backward walk

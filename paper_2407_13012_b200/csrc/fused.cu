@@ -36,15 +36,19 @@ struct SweepShape {
   int glo;     // global bit of local bit 3 (B sweeps)
 };
 
-std::vector<SweepShape> plan_sweeps(int n) {
+// sweeps applying gates to qubits [lo, hi] of an n-qubit array: an A sweep for the
+// part below 12, then 9-qubit B windows (the last window slides down to n-9)
+std::vector<SweepShape> plan_range(int n, int lo, int hi) {
   std::vector<SweepShape> out;
-  out.push_back({true, 0, std::min(n, kSweepT) - 1, 0});
-  for (int lo = kSweepT; lo < n; lo += 9) {
-    const int hi = std::min(lo + 8, n - 1);
-    out.push_back({false, lo, hi, std::min(lo, n - 9)});
+  if (lo < kSweepT) out.push_back({true, lo, std::min(hi, kSweepT - 1), 0});
+  for (int s = std::max(lo, kSweepT); s <= hi; s += 9) {
+    const int e = std::min(s + 8, hi);
+    out.push_back({false, s, e, std::min(s, n - 9)});
   }
   return out;
 }
+
+std::vector<SweepShape> plan_sweeps(int n) { return plan_range(n, 0, n - 1); }
 
 // register-bit family of the fast sweeps (QSB_SWEEP_R1 / QSB_SWEEP_R2 override)
 int sweep_family(int nv) {
@@ -377,6 +381,59 @@ int forward_fused(Runner& R, double2* amps, int p, const double* gammas, const d
 }
 
 int upper_sweeps(int n, int p) { return 2 * p * (int)plan_sweeps(n).size() + 4; }
+
+}  // namespace
+
+extern "C" {
+
+// Gates Rx(theta) on qubits [lo, hi] of n-qubit array(s) v0 (and v1 when nv == 2),
+// with the fused ops in `flags` (QSB_SW_*): pre ops on the first sweep, post ops and
+// NO_STORE on the last, XSUM on all.  sums[0..2] = {<C> or post <bra|C|ket>, pre
+// <bra|C|ket>, sum_j <bra|X_j|ket>} (imaginary parts for the bra/ket contractions).
+// Building block of the sharded walk (dist.py): the gates of one layer are split
+// around the index-bit swap.
+int qsb_layer_sweeps(qsb_ctx* ctx, qsb_table* t, double* v0, double* v1, int nv, int n, int lo, int hi,
+                     double theta, unsigned flags, double phase_scale, double* sums) {
+  if (!ctx || !t || !v0 || (nv == 2 && !v1) || !sums) return invalid("qsb_layer_sweeps: null argument");
+  if (nv != 1 && nv != 2) return invalid("qsb_layer_sweeps: nv must be 1 or 2");
+  if (n < kSweepT || n > 62 || n != t->n) return invalid("qsb_layer_sweeps: n=%d (table n=%d, need >= 12)", n, t->n);
+  if (lo < 0 || hi >= n || lo > hi) return invalid("qsb_layer_sweeps: bad qubit range [%d, %d]", lo, hi);
+  const bool exact = flags & QSB_SW_EXACT;
+  Runner R{ctx, t, n, exact};
+  R.shapes = plan_range(n, lo, hi);
+  unsigned g1 = ctx->num_sms;
+  R.maxgrid = (unsigned)std::min<uint64_t>(g1, 1ull << (n - kSweepT));
+  QSB_TRY(ensure_scratch(ctx, (uint64_t)(R.shapes.size() + 1) * kSlots * R.maxgrid * sizeof(double) + 64));
+  R.partials = ctx->d_scratch;
+  const double2* lut = nullptr;
+  if ((flags & QSB_SW_PRE_PHASE) && t->kind != 0) {
+    QSB_TRY(prepare_luts(t, {phase_scale}, {make_double2(1.0, 0.0)}, exact));
+    lut = t->d_lut;
+  }
+  const Gate g = make_gate(theta, exact);
+  const uint32_t pre = flags & (QSB_SW_PLUS | QSB_SW_PRE_PHASE | QSB_SW_BRA_FROM_KET | QSB_SW_PRE_DINNER);
+  const uint32_t post = flags & (QSB_SW_POST_EXPECT | QSB_SW_POST_DINNER | QSB_SW_NO_STORE);
+  const int ns = (int)R.shapes.size();
+  for (int s = 0; s < ns; ++s) {
+    uint32_t f = flags & QSB_SW_XSUM;
+    if (s == 0) f |= pre;
+    if (s == ns - 1) f |= post;
+    QSB_TRY(R.sweep(nv, R.shapes[s], (double2*)v0, (double2*)v1, g, f, s == 0 ? lut : nullptr, phase_scale,
+                    make_double2(1.0, 0.0), true, nullptr));
+  }
+  std::vector<double> h;
+  QSB_TRY(R.fetch(h));
+  for (int k = 0; k < kSlots; ++k) {
+    double acc = 0.0;
+    for (int sw = 0; sw < ns; ++sw) acc += Runner::slot_sum(h, R.maxgrid, R.grids, sw, k);
+    sums[k] = acc;
+  }
+  return QSB_OK;
+}
+
+}  // extern "C"
+
+namespace {
 
 }  // namespace
 

@@ -21,12 +21,28 @@ constexpr int kPreThreads = 256;
 constexpr int kPreX = 4;            // x values per thread
 constexpr int kTermChunk = 2048;    // terms staged in shared memory per pass
 
+// Shard index map (sharded statevectors): local index i -> global assignment
+// x = (i & (2^b - 1)) | (rank << s1) | ((i >> b) << s2).  Identity: b = 63, rank = 0.
+struct IndexMap {
+  uint32_t b, s1, s2;
+  uint64_t rank;
+  __host__ __device__ uint64_t operator()(uint64_t i) const {
+    const uint64_t lo = b >= 63 ? i : (i & ((1ull << b) - 1ull));
+    const uint64_t hi = b >= 63 ? 0 : ((i >> b) << s2);
+    return lo | (rank << s1) | hi;
+  }
+};
+
 __global__ void __launch_bounds__(kPreThreads) k_precompute(const double* __restrict__ w, const uint64_t* __restrict__ m,
-                                                            uint64_t num_terms, double* __restrict__ out, uint64_t len) {
+                                                            uint64_t num_terms, double* __restrict__ out, uint64_t len,
+                                                            IndexMap map) {
   __shared__ double sw[kTermChunk];
   __shared__ uint64_t sm[kTermChunk];
-  const uint64_t x0 = ((uint64_t)blockIdx.x * kPreThreads + threadIdx.x) * kPreX;
+  const uint64_t i0 = ((uint64_t)blockIdx.x * kPreThreads + threadIdx.x) * kPreX;
+  // the 4 indices of a thread (and the 128 of a warp, when b >= 7) map to consecutive x
+  const uint64_t x0 = map(i0);
   // warp-common high bits (bits >= 7 are equal for all x of this warp)
+  const bool skip_ok = map.b >= 7;
   const uint64_t warp_x = x0 & ~127ull;
   double acc[kPreX];
 #pragma unroll
@@ -41,20 +57,20 @@ __global__ void __launch_bounds__(kPreThreads) k_precompute(const double* __rest
     __syncthreads();
     for (int k = 0; k < cn; ++k) {
       const uint64_t mk = sm[k];
-      if ((mk & ~127ull) & ~warp_x) continue;  // warp-uniform: no x in this warp matches
+      if (skip_ok && ((mk & ~127ull) & ~warp_x)) continue;  // warp-uniform: no x in this warp matches
       const double wk = sw[k];
 #pragma unroll
       for (int e = 0; e < kPreX; ++e)
         if (((x0 + e) & mk) == mk) acc[e] = __dadd_rn(acc[e], wk);
     }
   }
-  if (x0 + kPreX <= len) {
-    double2* o = (double2*)(out + x0);
+  if (i0 + kPreX <= len) {
+    double2* o = (double2*)(out + i0);
     o[0] = make_double2(acc[0], acc[1]);
     o[1] = make_double2(acc[2], acc[3]);
   } else {
     for (int e = 0; e < kPreX; ++e)
-      if (x0 + e < len) out[x0 + e] = acc[e];
+      if (i0 + e < len) out[i0 + e] = acc[e];
   }
 }
 
@@ -79,7 +95,7 @@ namespace qsb {
 int minmax(qsb_ctx* ctx, const double* v, uint64_t len, double* mn, double* mx);  // ops.cu
 
 static int precompute_into(qsb_ctx* ctx, const double* weights, const int64_t* masks, uint64_t num_terms,
-                           double* out, uint64_t len) {
+                           double* out, uint64_t len, IndexMap map = IndexMap{63, 63, 0, 0}) {
   const uint64_t tbytes = num_terms * (sizeof(double) + sizeof(uint64_t));
   QSB_TRY(ensure_small(ctx, tbytes + 64));
   double* dw = (double*)ctx->d_small;
@@ -91,7 +107,7 @@ static int precompute_into(qsb_ctx* ctx, const double* weights, const int64_t* m
   }
   const uint64_t threads_needed = (len + kPreX - 1) / kPreX;
   const uint64_t blocks = (threads_needed + kPreThreads - 1) / kPreThreads;
-  k_precompute<<<(unsigned)blocks, kPreThreads, 0, ctx->stream>>>(dw, dm, num_terms, out, len);
+  k_precompute<<<(unsigned)blocks, kPreThreads, 0, ctx->stream>>>(dw, dm, num_terms, out, len, map);
   QSB_CHECK_LAUNCH(ctx, "precompute");
   QSB_CUDA(cudaStreamSynchronize(ctx->stream));  // host term arrays / d_small reuse
   return QSB_OK;
@@ -185,6 +201,23 @@ int qsb_table_create(qsb_ctx* ctx, int n, const double* weights, const int64_t* 
     if (masks[k] < 0 || (uint64_t)masks[k] >= len) return invalid("term mask %lld out of range for n=%d", (long long)masks[k], n);
   QSB_TRY(precompute_into(ctx, weights, masks, num_terms, values, len));
   return qsb_table_wrap(ctx, n, values, min_out, max_out, out);
+}
+
+// Shard of a 2^n_global table: local index i of `rank` under the layout map
+// x = (i & (2^b-1)) | (rank << s1) | ((i >> b) << s2) (see dist.py for the layouts).
+int qsb_table_create_mapped(qsb_ctx* ctx, int n_global, int n_local, const double* weights, const int64_t* masks,
+                            uint64_t num_terms, int b, int s1, int s2, uint64_t rank, double* values, double* min_out,
+                            double* max_out, qsb_table** out) {
+  if (!ctx || !values || !out) return invalid("qsb_table_create_mapped: null argument");
+  if (n_local < 1 || n_local > n_global || n_global > 62) return invalid("bad shard geometry %d/%d", n_local, n_global);
+  const uint64_t glen = 1ull << n_global;
+  for (uint64_t k = 0; k < num_terms; ++k)
+    if (masks[k] < 0 || (uint64_t)masks[k] >= glen)
+      return invalid("term mask %lld out of range for n=%d", (long long)masks[k], n_global);
+  if (b < 2 || b > n_local) return invalid("index map needs 2 <= b <= n_local (b=%d)", b);
+  IndexMap map{(uint32_t)b, (uint32_t)s1, (uint32_t)s2, rank};
+  QSB_TRY(precompute_into(ctx, weights, masks, num_terms, values, 1ull << n_local, map));
+  return qsb_table_wrap(ctx, n_local, values, min_out, max_out, out);
 }
 
 int qsb_table_wrap(qsb_ctx* ctx, int n, double* values, double* min_out, double* max_out, qsb_table** out) {

@@ -1,0 +1,311 @@
+"""Sharded statevectors across G = 2^g GPUs (future work in the
+reference, PAPER.md:234 / SPEC.md:155).
+
+Shard r of an n-qubit state holds N_l = 2^(n-g) amplitudes.  Two layouts alternate:
+
+  layout A: local index i <-> global x = i | (r << n_l)
+  layout B: the top g local bits and the rank bits trade places:
+            x = (i & (2^(n_l-g)-1)) | (r << (n_l-g)) | ((i >> (n_l-g)) << n_l)
+
+Going A <-> B is one all-to-all of equal contiguous chunks (chunk c of shard r, i.e.
+the amplitudes whose top g local bits are c, goes to shard c and lands as its chunk
+r) — `torch.distributed.all_to_all_single` over NCCL/NVLink with one shard per
+process, or device copies when several virtual shards share one GPU (tests).
+
+Every layer's mixer is Rx(theta) on *every* qubit, so which qubit sits at which
+position does not matter for the gates: a layer applies the phase (table of the
+current layout) and Rx to all n_l local positions, swaps, then applies Rx to the g
+positions that just arrived.  The next layer starts in the other layout.  The
+adjoint walk does the same with the bra/ket pair; the fused contractions
+(<C>, <bra|C|ket>, sum_j <bra|X_j|ket>) are per-shard partial sums combined in rank
+order.  `program()` is that schedule as data, executed on the GPU by `_run` and
+emulated in numpy by the tests (tests/test_dist_host.py).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib, backend, circuit, costpoly
+from ._lib import DeviceArray, call
+from .errors import ContractViolation
+from .kernels import b200
+
+# fused-op flags of qsb_layer_sweeps (include/qsb.h)
+PLUS, PRE_PHASE, BRA_FROM_KET, PRE_DINNER, XSUM, POST_EXPECT, POST_DINNER, NO_STORE = (
+    1, 2, 4, 8, 16, 32, 64, 128)
+EXACT = 65536
+
+
+# ---------------------------------------------------------------- layouts
+def index_map(layout: int, n: int, g: int, rank: int) -> tuple[int, int, int, int]:
+    """(b, s1, s2, rank) such that x = (i & (2^b-1)) | (rank << s1) | ((i >> b) << s2)."""
+    n_l = n - g
+    if layout == 0:
+        return n_l, n_l, 0, rank
+    return n_l - g, n_l - g, n_l, rank
+
+
+def global_index(layout: int, n: int, g: int, rank: int, i: np.ndarray) -> np.ndarray:
+    b, s1, s2, r = index_map(layout, n, g, rank)
+    i = np.asarray(i, dtype=np.int64)
+    return (i & ((1 << b) - 1)) | (r << s1) | ((i >> b) << s2)
+
+
+# ---------------------------------------------------------------- the schedule
+@dataclass(frozen=True)
+class Sweeps:
+    nv: int            # 1: ket only, 2: bra and ket
+    lo: int            # gated local positions [lo, hi]
+    hi: int
+    theta: float       # Rx(theta)
+    flags: int
+    phase: float       # exp(i * phase * C) before the gates when PRE_PHASE
+    layer: int         # QAOA layer index (0-based)
+    tag: str           # "fwd" / "fwd_tail" / "bwd" / "bwd_tail"
+
+
+@dataclass(frozen=True)
+class Swap:
+    nv: int
+
+
+def program(n: int, g: int, gammas, betas, want_value: bool, want_grad: bool):
+    """The sharded forward (+ adjoint) walk as a list of Sweeps / Swap steps."""
+    n_l = n - g
+    p = len(gammas)
+    steps: list = []
+    for i in range(p):
+        f = PRE_PHASE | (PLUS if i == 0 else 0)
+        steps.append(Sweeps(1, 0, n_l - 1, -2.0 * betas[i], f, -gammas[i], i, "fwd"))
+        steps.append(Swap(1))
+        tail = POST_EXPECT if (i == p - 1 and want_value) else 0
+        steps.append(Sweeps(1, n_l - g, n_l - 1, -2.0 * betas[i], tail, 0.0, i, "fwd_tail"))
+    if not want_grad:
+        return steps
+    for i in range(p - 1, -1, -1):
+        f = XSUM | (BRA_FROM_KET if i == p - 1 else PRE_DINNER | PRE_PHASE)
+        ph = gammas[i + 1] if i < p - 1 else 0.0
+        steps.append(Sweeps(2, 0, n_l - 1, 2.0 * betas[i], f, ph, i, "bwd"))
+        steps.append(Swap(2))
+        tail = XSUM | ((POST_DINNER | NO_STORE) if i == 0 else 0)
+        steps.append(Sweeps(2, n_l - g, n_l - 1, 2.0 * betas[i], tail, 0.0, i, "bwd_tail"))
+    return steps
+
+
+def collect(steps, sums_per_step, p: int):
+    """Fold per-step contraction sums (already combined over shards) into
+    (value, d_gammas, d_betas) exactly as the single-GPU walk defines them."""
+    value = None
+    dg = np.zeros(p)
+    db = np.zeros(p)
+    xs = np.zeros(p)
+    for st, s in zip(steps, sums_per_step):
+        if not isinstance(st, Sweeps):
+            continue
+        if st.nv == 1 and (st.flags & POST_EXPECT):
+            value = s[0]
+        if st.nv == 2:
+            xs[st.layer] += s[2]
+            if st.flags & PRE_DINNER:
+                dg[st.layer + 1] = 2.0 * s[1]
+            if st.flags & POST_DINNER:
+                dg[st.layer] = 2.0 * s[0]
+    db[:] = -2.0 * xs
+    return value, dg, db
+
+
+# ---------------------------------------------------------------- exchangers
+class VirtualExchanger:
+    """All G shards live in this process on one device: the all-to-all is G^2 chunk copies."""
+
+    def __init__(self, g: int):
+        self.G = 1 << g
+        self.ranks = list(range(self.G))
+
+    def combine(self, per_rank_sums: list[np.ndarray]) -> np.ndarray:
+        total = np.zeros_like(per_rank_sums[0])
+        for s in per_rank_sums:  # rank order: deterministic
+            total = total + s
+        return total
+
+    def swap(self, vecs: list[DeviceArray], scratch: list[DeviceArray]) -> None:
+        G = self.G
+        chunk = len(vecs[0]) // G
+        nbytes = chunk * 16
+        for r in range(G):
+            for c in range(G):
+                call("qsb_d2d", vecs[r].dctx.handle, scratch[c].ptr + r * nbytes, vecs[r].ptr + c * nbytes, nbytes)
+        for k in range(G):  # the received data becomes the state; the old state the scratch
+            vecs[k].ptr, scratch[k].ptr = scratch[k].ptr, vecs[k].ptr
+
+
+class TorchExchanger:
+    """One shard per process (torchrun): NCCL all-to-all over NVLink/NVSwitch."""
+
+    def __init__(self, g: int, dist, device: int):
+        self.G = 1 << g
+        self.dist = dist
+        self.rank = dist.get_rank()
+        self.ranks = [self.rank]
+        self.device = device
+        if dist.get_world_size() != self.G:
+            raise ContractViolation(f"world size {dist.get_world_size()} != 2^g = {self.G}")
+
+    def combine(self, per_rank_sums: list[np.ndarray]) -> np.ndarray:
+        import torch
+
+        mine = torch.tensor(per_rank_sums[0], dtype=torch.float64, device=f"cuda:{self.device}")
+        out = [torch.empty_like(mine) for _ in range(self.G)]
+        self.dist.all_gather(out, mine)
+        total = np.zeros_like(per_rank_sums[0])
+        for t in out:  # rank order: deterministic, identical on every rank
+            total = total + t.cpu().numpy()
+        return total
+
+    def swap(self, vecs: list[DeviceArray], scratch: list[DeviceArray]) -> None:
+        import torch
+
+        v, s = vecs[0], scratch[0]
+        v.dctx.sync()  # our stream -> NCCL's stream
+        src = torch.as_tensor(_CudaView(v), device=f"cuda:{self.device}").view(self.G, -1)
+        dst = torch.as_tensor(_CudaView(s), device=f"cuda:{self.device}").view(self.G, -1)
+        self.dist.all_to_all_single(dst, src)
+        torch.cuda.synchronize(self.device)
+        v.ptr, s.ptr = s.ptr, v.ptr
+
+
+class _CudaView:
+    """__cuda_array_interface__ view of a DeviceArray as float64 pairs (no copy)."""
+
+    def __init__(self, d: DeviceArray):
+        self.__cuda_array_interface__ = {
+            "shape": (2 * d.length,) if d.dtype == np.complex128 else (d.length,),
+            "typestr": "<f8",
+            "data": (d.ptr, False),
+            "version": 3,
+            "strides": None,
+            "stream": None,
+        }
+
+
+# ---------------------------------------------------------------- sharded handle
+class ShardedHandle:
+    """A polynomial's statevector split over 2^g shards (this process holds
+    `exchanger.ranks`), with cost tables for both layouts."""
+
+    def __init__(self, poly: costpoly.Polynomial, g: int, exchanger, device: int | None = None):
+        n = poly.n
+        if g < 1:
+            raise ContractViolation("sharding needs g >= 1 (use create_handle for one GPU)")
+        if n - g < 12:
+            raise ContractViolation(f"shards need >= 12 local qubits (n={n}, g={g})")
+        self.n, self.g, self.n_l = n, g, n - g
+        self.poly = poly
+        self.ex = exchanger
+        if device is not None:
+            import os
+
+            os.environ["QAOA_DEVICE"] = str(device)
+        self.ctx = backend.create_context("b200")
+        dctx = self.ctx.device
+        N_l = 1 << self.n_l
+        self.ranks = list(exchanger.ranks)
+        self.ket = [DeviceArray(dctx, N_l, np.complex128) for _ in self.ranks]
+        self.bra = [DeviceArray(dctx, N_l, np.complex128) for _ in self.ranks]
+        self.scratch = [DeviceArray(dctx, N_l, np.complex128) for _ in self.ranks]
+        w = np.ascontiguousarray(poly.weights, dtype=np.float64)
+        m = np.ascontiguousarray(poly.masks, dtype=np.int64)
+        self.tables = [[None] * len(self.ranks), [None] * len(self.ranks)]
+        lo, hi = np.inf, -np.inf
+        for layout in (0, 1):
+            for k, r in enumerate(self.ranks):
+                vals = DeviceArray(dctx, N_l, np.float64)
+                b, s1, s2, rank = index_map(layout, n, g, r)
+                mn, mx, ptr = C.c_double(), C.c_double(), C.c_void_p()
+                call("qsb_table_create_mapped", dctx.handle, n, self.n_l, w.ctypes.data, m.ctypes.data, w.shape[0],
+                     b, s1, s2, rank, vals.ptr, C.byref(mn), C.byref(mx), C.byref(ptr))
+                b200._attach(vals, ptr)
+                self.tables[layout][k] = vals
+                lo, hi = min(lo, mn.value), max(hi, mx.value)
+        self.min_value, self.max_value = self._minmax(lo, hi)
+        self.layout = 0
+
+    def _minmax(self, lo: float, hi: float) -> tuple[float, float]:
+        if isinstance(self.ex, VirtualExchanger):
+            return lo, hi
+        import torch
+
+        t = torch.tensor([-lo, hi], dtype=torch.float64, device=f"cuda:{self.ex.device}")
+        self.ex.dist.all_reduce(t, op=self.ex.dist.ReduceOp.MAX)
+        return -float(t[0]), float(t[1])
+
+    # -- execution
+    def _run(self, steps, exact: bool) -> list[np.ndarray]:
+        layout = 0
+        sums_per_step = []
+        for st in steps:
+            if isinstance(st, Swap):
+                self.ex.swap(self.ket, self.scratch)
+                if st.nv == 2:
+                    self.ex.swap(self.bra, self.scratch)
+                layout ^= 1
+                sums_per_step.append(None)
+                continue
+            per = []
+            for k in range(len(self.ranks)):
+                out = (C.c_double * 3)()
+                table = self.tables[layout][k]
+                call("qsb_layer_sweeps", self.ctx.device.handle, table.table.ptr, self.ket[k].ptr,
+                     self.bra[k].ptr if st.nv == 2 else None, st.nv, self.n_l, st.lo, st.hi, float(st.theta),
+                     st.flags | (EXACT if exact else 0), float(st.phase), out)
+                per.append(np.array(out[:3]))
+            sums_per_step.append(per)
+        # one combine for the whole walk: stack every step's per-shard sums
+        idx = [i for i, s in enumerate(sums_per_step) if s is not None]
+        stacked = [np.concatenate([sums_per_step[i][k] for i in idx]) for k in range(len(self.ranks))]
+        total = self.ex.combine(stacked) if stacked else np.zeros(0)
+        out = [None] * len(steps)
+        for j, i in enumerate(idx):
+            out[i] = total[3 * j: 3 * j + 3]
+        self.layout = layout
+        return out
+
+    def value_and_grad(self, params: circuit.QaoaParams, exact: bool = False):
+        if params.p < 1:
+            raise ContractViolation("gradient needs depth p >= 1")
+        steps = program(self.n, self.g, params.gammas, params.betas, True, True)
+        value, dg, db = collect(steps, self._run(steps, exact), params.p)
+        return self._clamp(value), dg, db
+
+    def expectation(self, params: circuit.QaoaParams, exact: bool = False) -> float:
+        if params.p < 1:
+            raise ContractViolation("sharded expectation needs p >= 1")
+        steps = program(self.n, self.g, params.gammas, params.betas, True, False)
+        value, _, _ = collect(steps, self._run(steps, exact), params.p)
+        return self._clamp(value)
+
+    def _clamp(self, v: float) -> float:
+        return min(max(v, self.min_value), self.max_value)
+
+    def gather_state(self) -> np.ndarray:
+        """Full statevector in global index order (virtual shards, tests)."""
+        if not isinstance(self.ex, VirtualExchanger):
+            raise ContractViolation("gather_state needs all shards in this process")
+        out = np.empty(1 << self.n, dtype=np.complex128)
+        i = np.arange(1 << self.n_l, dtype=np.int64)
+        for k, r in enumerate(self.ranks):
+            out[global_index(self.layout, self.n, self.g, r, i)] = self.ket[k].to_host()
+        return out
+
+    def simulate(self, params: circuit.QaoaParams, exact: bool = False) -> None:
+        steps = program(self.n, self.g, params.gammas, params.betas, False, False)
+        self._run(steps, exact)
+
+    def close(self) -> None:
+        for arrs in (self.ket, self.bra, self.scratch, *self.tables):
+            for a in arrs:
+                a.free()
