@@ -150,8 +150,8 @@ int qsb_simulate_expect(qsb_ctx* ctx, qsb_table* t, double* amps, int p, const d
 int qsb_rx_layer(qsb_ctx* ctx, double* amps, int n, double theta, unsigned flags);
 /* Rx(theta) on qubits [lo, hi] with fused ops (QSB_SW_*); sums[3] = partial sums
  * (see fused.cu).  Building block of the sharded walk. */
-int qsb_layer_sweeps(qsb_ctx* ctx, qsb_table* t, double* v0, double* v1, int nv, int n, int lo, int hi,
-                     double theta, unsigned flags, double phase_scale, double* sums);
+int qsb_layer_sweeps(qsb_ctx* ctx, qsb_table* t, double* v0, double* v1, int nv, int n, int n_global, int lo,
+                     int hi, double theta, unsigned flags, double phase_scale, double* sums);
 /* <psi|C|psi> (circuit.expectation_of_state, circuit.py:106-113, without the clamp) */
 int qsb_expectation(qsb_ctx* ctx, qsb_table* t, const double* amps, unsigned flags, double* out);
 /* expectation + adjoint gradient (adjoint.py:37-77): one forward, one backward walk

@@ -72,7 +72,7 @@ _SIGS = {
     "qsb_table_wrap": [_vp, _i32, _vp, _dp, _dp, C.POINTER(_vp)],
     "qsb_table_create_mapped": [_vp, _i32, _i32, _vp, _vp, _u64, _i32, _i32, _i32, _u64, _vp, _dp, _dp,
                                 C.POINTER(_vp)],
-    "qsb_layer_sweeps": [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _dbl, C.c_uint, _dbl, _dp],
+    "qsb_layer_sweeps": [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _dbl, C.c_uint, _dbl, _dp],
     "qsb_table_destroy": [_vp],
     "qsb_table_kind": [_vp, C.POINTER(_i32), C.POINTER(_i32)],
     "qsb_table_phase": [_vp, _vp, _vp, _dbl],

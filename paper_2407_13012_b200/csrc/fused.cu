@@ -255,6 +255,7 @@ struct Runner {
   std::vector<unsigned> grids;  // per launched sweep
   int nsweeps_launched = 0;
   double* partials = nullptr;   // device, kSlots * maxgrid per sweep
+  double plus_amp = 0.0;        // 0: 1/sqrt(2^n)
   unsigned maxgrid = 0;
 
   int init(int total_sweeps_upper) {
@@ -312,7 +313,7 @@ struct Runner {
     a.form = g.form;
     a.ga = g.ga;
     a.gb = g.gb;
-    a.plus_amp = 1.0 / sqrt((double)(1ull << n));
+    a.plus_amp = plus_amp > 0.0 ? plus_amp : 1.0 / sqrt((double)(1ull << n));
     for (int p = 0; p < kMaxPhases; ++p) a.xs_w[p] = ipow(g.sigma * g.sigma, gbp[p]);
     a.post_scale = ipow(g.sigma, gates);
     if (!exact && gates > 0) flags |= SF_POST_SCALE;
@@ -392,14 +393,16 @@ extern "C" {
 // <bra|C|ket>, sum_j <bra|X_j|ket>} (imaginary parts for the bra/ket contractions).
 // Building block of the sharded walk (dist.py): the gates of one layer are split
 // around the index-bit swap.
-int qsb_layer_sweeps(qsb_ctx* ctx, qsb_table* t, double* v0, double* v1, int nv, int n, int lo, int hi,
-                     double theta, unsigned flags, double phase_scale, double* sums) {
+int qsb_layer_sweeps(qsb_ctx* ctx, qsb_table* t, double* v0, double* v1, int nv, int n, int n_global, int lo,
+                     int hi, double theta, unsigned flags, double phase_scale, double* sums) {
   if (!ctx || !t || !v0 || (nv == 2 && !v1) || !sums) return invalid("qsb_layer_sweeps: null argument");
   if (nv != 1 && nv != 2) return invalid("qsb_layer_sweeps: nv must be 1 or 2");
   if (n < kSweepT || n > 62 || n != t->n) return invalid("qsb_layer_sweeps: n=%d (table n=%d, need >= 12)", n, t->n);
   if (lo < 0 || hi >= n || lo > hi) return invalid("qsb_layer_sweeps: bad qubit range [%d, %d]", lo, hi);
+  if (n_global < n || n_global > 62) return invalid("qsb_layer_sweeps: n_global=%d < n=%d", n_global, n);
   const bool exact = flags & QSB_SW_EXACT;
   Runner R{ctx, t, n, exact};
+  R.plus_amp = 1.0 / sqrt((double)(1ull << n_global));  // |+> of the whole (sharded) register
   R.shapes = plan_range(n, lo, hi);
   unsigned g1 = ctx->num_sms;
   R.maxgrid = (unsigned)std::min<uint64_t>(g1, 1ull << (n - kSweepT));

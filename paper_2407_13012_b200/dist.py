@@ -260,7 +260,7 @@ class ShardedHandle:
                 out = (C.c_double * 3)()
                 table = self.tables[layout][k]
                 call("qsb_layer_sweeps", self.ctx.device.handle, table.table.ptr, self.ket[k].ptr,
-                     self.bra[k].ptr if st.nv == 2 else None, st.nv, self.n_l, st.lo, st.hi, float(st.theta),
+                     self.bra[k].ptr if st.nv == 2 else None, st.nv, self.n_l, self.n, st.lo, st.hi, float(st.theta),
                      st.flags | (EXACT if exact else 0), float(st.phase), out)
                 per.append(np.array(out[:3]))
             sums_per_step.append(per)
