@@ -139,6 +139,11 @@ int build_shape(const SweepShape& sh, int n, int nv, bool exact, SweepArgs& a, i
     add_run(sh.glo + 9, n - sh.glo - 9);
   }
   a.ntiles = 1ull << (n - kSweepT);
+  // whole window targeted -> the kernel uses the compile-time masks (shape_apply)
+  a.full = sh.is_a ? (sh.lo == 0 && sh.hi == kSweepT - 1) : (sh.lo == sh.glo && sh.hi == sh.glo + 8);
+  if (a.full)
+    for (int p = 0; p < np; ++p)
+      if (a.ph[p].apply != shape_apply(shape, p)) return -1;  // planner and kernel must agree
   return gates;
 }
 

@@ -65,6 +65,7 @@ struct SweepArgs {
   int cshift;             // global bit of local bit 3 (cidx 8-entry chunk c -> base + (c << cshift))
   int shape;              // SweepShapeId
   int cmode;              // compact index tile in smem: 0 none, 1 natural order, 2 B-tile u8 (16-wide rows)
+  int full;               // every window position is a target: gate masks are compile-time (shape_apply)
   int glo;                // B shapes: global bit of local bit 3
   PhaseMap ld;            // cp.async load mapping: lanes <-> local 0..4 (coalesced)
   PhaseMap ph[kMaxPhases];
@@ -126,6 +127,24 @@ __host__ __device__ constexpr PhaseSpec shape_phase(int sh, int p) {
                       : p == 1 ? PhaseSpec{{0, 1, 2, 3, 4}, {5, 9, 10, 11}, 6, true}
                       :          PhaseSpec{{0, 1, 2, 3, 4}, {5, 6, 7, 8}, 9, true});
   // clang-format on
+}
+
+// Gate mask of phase p when the whole window is targeted: register bits that are a
+// register bit for the first time (and the phase is allowed to apply gates).
+__host__ __device__ constexpr uint32_t shape_apply(int sh, int p) {
+  uint32_t m = 0;
+  const PhaseSpec P = shape_phase(sh, p);
+  if (!P.allow) return 0;
+  for (int b = 0; b < shape_r(sh); ++b) {
+    const int loc = P.reg_l + b;
+    bool seen = false;
+    for (int q = 0; q < p; ++q) {
+      const PhaseSpec Q = shape_phase(sh, q);
+      if (Q.allow && loc >= Q.reg_l && loc < Q.reg_l + shape_r(sh)) seen = true;
+    }
+    if (!seen) m |= 1u << b;
+  }
+  return m;
 }
 
 // family r in {5, 4, 3} for fast mode; exact mode always uses the R=4 shapes

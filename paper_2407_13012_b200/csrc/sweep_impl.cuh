@@ -143,8 +143,9 @@ __device__ __forceinline__ void butterfly(double2& t, double2& u, double ga, dou
 
 // ------------------------------------------------------------------ kernel
 // SH: shape, NV: vectors (1 or 2), FORM: gate arithmetic, KSIN: f64 table +
-// device sincos for the A-shape pre ops (else compact index + LUT).
-template <int SH, int NV, int FORM, bool KSIN>
+// device sincos (else compact index + LUT), FULL: every window position is a
+// target (gate masks fixed at compile time by the shape).
+template <int SH, int NV, int FORM, bool KSIN, bool FULL>
 __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_constant__ SweepArgs a) {
   constexpr int R = shape_r(SH), W = shape_w(SH), NP = shape_np(SH);
   constexpr bool IS_A = shape_is_a(SH);
@@ -223,12 +224,6 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
   double acc0 = 0.0, acc0b = 0.0, acc1 = 0.0, acc1b = 0.0, acc2 = 0.0;
   double2 v[NV][NR];
 
-  // cost value of local index l (global index g): compact index tile in smem, or the f64 table
-  auto cval = [&](const uint8_t* cs, uint32_t tb8, uint32_t l, uint64_t g) -> double {
-    if (cmode == 0) return a.table[g];
-    if (cmode == 2) return a.vmin + (double)cs[((l >> 3) << 4) | tb8 | (l & 7u)];
-    return a.vmin + (double)(a.kind == 1 ? cs[l] : ((const uint16_t*)cs)[l]);
-  };
 
   issue(0);
   issue(1);
@@ -240,17 +235,18 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
     uint32_t lb = lbase<W>(P0, lane, warp);
     uint32_t xs_addr;  // byte address of the exchange slot for this tile
 
+    // Loads are unconditional (a skipped TMA leaves stale data that is overwritten
+    // below): no branch around the register tile, hence no phi-moves of it.
     if constexpr (NV == 1) {
       issue(k + 2);
       wait_seq(k);
       xs_addr = ring_s + (uint32_t)(k % kRing) * kSlotBytes;
-      if (flags & SF_PLUS) {
+      const uint32_t p0 = xs_addr + lb * 16u;  // natural (TMA) layout
+      const bool plus = flags & SF_PLUS;
 #pragma unroll
-        for (int j = 0; j < NR; ++j) v[0][j] = make_double2(a.plus_amp, 0.0);
-      } else {
-        const uint32_t p0 = xs_addr + lb * 16u;  // natural (TMA) layout
-#pragma unroll
-        for (int j = 0; j < NR; ++j) v[0][j] = lds(p0 + (((uint32_t)j << P0.reg_l) * 16u));
+      for (int j = 0; j < NR; ++j) {
+        const double2 x = lds(p0 + (((uint32_t)j << P0.reg_l) * 16u));
+        v[0][j] = make_double2(plus ? a.plus_amp : x.x, plus ? 0.0 : x.y);
       }
     } else {
       issue(2 * k + 2);  // bra of the next tile into the slot freed at the end of tile k-1
@@ -258,11 +254,9 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
       wait_seq(2 * k + 1);
       const uint32_t b_addr = ring_s + (uint32_t)((2 * k) % kRing) * kSlotBytes;
       xs_addr = ring_s + (uint32_t)((2 * k + 1) % kRing) * kSlotBytes;
-      if (!(flags & SF_BRA_FROM_KET)) {
-        const uint32_t p0 = b_addr + lb * 16u;
+      const uint32_t pb = b_addr + lb * 16u;
 #pragma unroll
-        for (int j = 0; j < NR; ++j) v[1][j] = lds(p0 + (((uint32_t)j << P0.reg_l) * 16u));
-      }
+      for (int j = 0; j < NR; ++j) v[1][j] = lds(pb + (((uint32_t)j << P0.reg_l) * 16u));
       fence_proxy_async();
       __syncthreads();
       issue(2 * k + 3);  // ket of the next tile into the bra slot just read
@@ -272,39 +266,94 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
     }
 
     // ---------------------------------------------------------------- pre ops
-    if (flags & (SF_PRE_PHASE | SF_BRA_FROM_KET | SF_PRE_DINNER)) {
+    // table-kind dispatch hoisted out of the unrolled loops (tv: value / phase views)
+    auto pre_ops = [&](auto tv) {
       const uint64_t g0 = base + gofs<IS_A>(lb, glo);
+      if constexpr (NV == 2) {
+        if (flags & SF_BRA_FROM_KET) {
 #pragma unroll
-      for (int j = 0; j < NR; ++j) {
-        const uint32_t l = lb | ((uint32_t)j << P0.reg_l);
-        const uint64_t g = g0 + gofs<IS_A>((uint32_t)j << P0.reg_l, glo);
-        double t = 0.0;
-        if (flags & (SF_BRA_FROM_KET | SF_PRE_DINNER)) t = cval(cs, tb8, l, g);
-        if constexpr (NV == 2) {
-          if (flags & SF_BRA_FROM_KET) v[1][j] = make_double2(t * v[0][j].x, t * v[0][j].y);
-          if (flags & SF_PRE_DINNER) {
+          for (int j = 0; j < NR; ++j) {
+            const double t = tv.val(lb | ((uint32_t)j << P0.reg_l), g0 + gofs<IS_A>((uint32_t)j << P0.reg_l, glo));
+            v[1][j] = make_double2(t * v[0][j].x, t * v[0][j].y);
+          }
+        }
+        if (flags & SF_PRE_DINNER) {
+#pragma unroll
+          for (int j = 0; j < NR; ++j) {
+            const double t = tv.val(lb | ((uint32_t)j << P0.reg_l), g0 + gofs<IS_A>((uint32_t)j << P0.reg_l, glo));
             const double d = v[1][j].x * v[0][j].y - v[1][j].y * v[0][j].x;
             if (j & 1) acc1b = fma(t, d, acc1b);
             else acc1 = fma(t, d, acc1);
           }
         }
-        if (flags & SF_PRE_PHASE) {
-          double2 f;
-          if constexpr (KSIN) {
-            double sn, cn;
-            sincos(a.pre_ang * a.table[g], &sn, &cn);
-            f = make_double2(cn, sn);
-            if constexpr (!EXACT) f = cmul_fast(f, a.pre_extra);
-          } else if (cmode == 2) {
-            f = slut[cs[((l >> 3) << 4) | tb8 | (l & 7u)]];
-          } else {
-            f = a.kind == 1 ? slut[cs[l]] : __ldg(&a.lut[((const uint16_t*)cs)[l]]);
-          }
+      }
+      if (flags & SF_PRE_PHASE) {
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+          const double2 f = tv.phase(lb | ((uint32_t)j << P0.reg_l), g0 + gofs<IS_A>((uint32_t)j << P0.reg_l, glo));
 #pragma unroll
           for (int q = 0; q < NV; ++q) v[q][j] = cmul<EXACT>(v[q][j], f);
         }
       }
-    }
+    };
+    // post ops: <psi|C|psi> (NV=1) or <bra|C|ket> (NV=2) after the gates, in the last map
+    constexpr int RL = shape_phase(SH, NP - 1).reg_l;
+    auto post_ops = [&](auto tv, uint32_t lbl) {
+      const uint64_t g1 = base + gofs<IS_A>(lbl, glo);
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        const double t = tv.val(lbl | ((uint32_t)j << RL), g1 + gofs<IS_A>((uint32_t)j << RL, glo));
+        double d;
+        if constexpr (NV == 1) d = fma(v[0][j].x, v[0][j].x, v[0][j].y * v[0][j].y);
+        else d = v[1][j].x * v[0][j].y - v[1][j].y * v[0][j].x;  // slot 0: PRE_DINNER may use slot 1
+        if (j & 1) acc0b = fma(t, d, acc0b);
+        else acc0 = fma(t, d, acc0);
+      }
+    };
+    struct TvF64 {  // f64 table from HBM, device sincos
+      const SweepArgs& a;
+      __device__ double val(uint32_t, uint64_t g) const { return a.table[g]; }
+      __device__ double2 phase(uint32_t, uint64_t g) const {
+        double sn, cn;
+        sincos(a.pre_ang * a.table[g], &sn, &cn);
+        double2 f = make_double2(cn, sn);
+        if constexpr (!EXACT) f = cmul_fast(f, a.pre_extra);
+        return f;
+      }
+    };
+    struct TvU8 {  // u8 index tile in natural order, LUT in smem
+      const SweepArgs& a;
+      const uint8_t* cs;
+      const double2* slut;
+      __device__ double val(uint32_t l, uint64_t) const { return a.vmin + (double)cs[l]; }
+      __device__ double2 phase(uint32_t l, uint64_t) const { return slut[cs[l]]; }
+    };
+    struct TvU16 {  // u16 index tile, LUT in HBM (L1-cached)
+      const SweepArgs& a;
+      const uint16_t* cs;
+      __device__ double val(uint32_t l, uint64_t) const { return a.vmin + (double)cs[l]; }
+      __device__ double2 phase(uint32_t l, uint64_t) const { return __ldg(&a.lut[cs[l]]); }
+    };
+    struct TvU8Rows {  // u8 index of a B tile: 16-wide rows, this tile's half at tb8
+      const SweepArgs& a;
+      const uint8_t* cs;
+      const double2* slut;
+      uint32_t tb8;
+      __device__ uint32_t at(uint32_t l) const { return ((l >> 3) << 4) | tb8 | (l & 7u); }
+      __device__ double val(uint32_t l, uint64_t) const { return a.vmin + (double)cs[at(l)]; }
+      __device__ double2 phase(uint32_t l, uint64_t) const { return slut[cs[at(l)]]; }
+    };
+    auto with_table = [&](auto&& fn) {
+      if constexpr (KSIN) {
+        fn(TvF64{a});
+      } else {
+        if (cmode == 2) fn(TvU8Rows{a, cs, slut, tb8});
+        else if (a.kind == 1) fn(TvU8{a, cs, slut});
+        else if (a.kind == 2) fn(TvU16{a, (const uint16_t*)cs});
+        else fn(TvF64{a});
+      }
+    };
+    if (flags & (SF_PRE_PHASE | SF_BRA_FROM_KET | SF_PRE_DINNER)) with_table([&](auto tv) { pre_ops(tv); });
 
     // ---------------------------------------------------------------- phases
 #pragma unroll
@@ -326,7 +375,8 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
         }
         lb = nlb;
       }
-      const uint32_t apply = a.ph[p].apply;
+      // FULL: compile-time gate mask (no branches around the register tile)
+      const uint32_t apply = FULL ? shape_apply(SH, p) : a.ph[p].apply;
       if constexpr (NV == 2) {
         // sum_j <bra|X_j|ket> for this phase's qubits, before any of its gates
         // (X_j commutes with every Rx): one scale factor xs_w[p] covers them
@@ -364,29 +414,16 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
     }
 
     // ---------------------------------------------------------------- post
-    constexpr int RL = shape_phase(SH, NP - 1).reg_l;
-    if constexpr (!EXACT) {
-      if (flags & SF_POST_SCALE) {
-        const double sc = a.post_scale;
+    if constexpr (!EXACT) {  // factored gates: one real scale per sweep (1.0 if no gates)
+      const double sc = a.post_scale;
 #pragma unroll
-        for (int q = 0; q < NV; ++q)
+      for (int q = 0; q < NV; ++q)
 #pragma unroll
-          for (int j = 0; j < NR; ++j) v[q][j] = make_double2(v[q][j].x * sc, v[q][j].y * sc);
-      }
+        for (int j = 0; j < NR; ++j) v[q][j] = make_double2(v[q][j].x * sc, v[q][j].y * sc);
     }
-    const uint64_t g1 = base + gofs<IS_A>(lb, glo);
-    if (flags & (SF_POST_EXPECT | SF_POST_DINNER)) {
-#pragma unroll
-      for (int j = 0; j < NR; ++j) {
-        const double t = cval(cs, tb8, lb | ((uint32_t)j << RL), g1 + gofs<IS_A>((uint32_t)j << RL, glo));
-        double d;
-        if constexpr (NV == 1) d = fma(v[0][j].x, v[0][j].x, v[0][j].y * v[0][j].y);
-        else d = v[1][j].x * v[0][j].y - v[1][j].y * v[0][j].x;  // slot 0: PRE_DINNER may use slot 1
-        if (j & 1) acc0b = fma(t, d, acc0b);
-        else acc0 = fma(t, d, acc0);
-      }
-    }
+    if (flags & (SF_POST_EXPECT | SF_POST_DINNER)) with_table([&](auto tv) { post_ops(tv, lb); });
     if (!(flags & SF_NO_STORE)) {
+      const uint64_t g1 = base + gofs<IS_A>(lb, glo);
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
         double2* dst = (q == 0 ? a.v0 : a.v1) + g1;
@@ -420,16 +457,16 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
   }
 }
 
-template <int SH, int NV, int FORM, bool KSIN>
+template <int SH, int NV, int FORM, bool KSIN, bool FULL>
 struct SweepKernel {
   static constexpr int threads = 32 << shape_w(SH);
   static int grid(qsb_ctx* ctx, uint64_t ntiles, unsigned* g) {
     static int occ = -1;  // per process; one device type
     if (occ < 0) {
-      QSB_CUDA(cudaFuncSetAttribute(k_sweep<SH, NV, FORM, KSIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      QSB_CUDA(cudaFuncSetAttribute(k_sweep<SH, NV, FORM, KSIN, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)kSmemBytes));
       int o = 0;
-      QSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sweep<SH, NV, FORM, KSIN>, threads, kSmemBytes));
+      QSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sweep<SH, NV, FORM, KSIN, FULL>, threads, kSmemBytes));
       occ = o < 1 ? 1 : o;
     }
     const uint64_t want = (uint64_t)ctx->num_sms * occ;
@@ -439,33 +476,44 @@ struct SweepKernel {
   static int launch(qsb_ctx* ctx, SweepArgs& a, unsigned* gout) {
     unsigned g;
     QSB_TRY(grid(ctx, a.ntiles, &g));
-    k_sweep<SH, NV, FORM, KSIN><<<g, threads, kSmemBytes, ctx->stream>>>(a);
+    k_sweep<SH, NV, FORM, KSIN, FULL><<<g, threads, kSmemBytes, ctx->stream>>>(a);
     QSB_CHECK_LAUNCH(ctx, "sweep");
     if (gout) *gout = g;
     return QSB_OK;
   }
 };
 
-// fast-mode instantiations of one register family (A shape SA, B shape SB)
+// fast-mode instantiations of one register family (A shape SA, B shape SB).  A
+// sweeps always cover their whole 12-bit window; B windows may be partial (FULL=0).
 template <int NV, int SA, int SB>
 int launch_fast(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
   auto L = [&](auto k) { return decltype(k)::launch(ctx, a, g); };
   const bool ksin = a.kind == 0;
   const bool c = a.form == GF_FACT_C;
   if (a.shape == SA) {
-    if (c) return ksin ? L(SweepKernel<SA, NV, GF_FACT_C, true>{}) : L(SweepKernel<SA, NV, GF_FACT_C, false>{});
-    return ksin ? L(SweepKernel<SA, NV, GF_FACT_S, true>{}) : L(SweepKernel<SA, NV, GF_FACT_S, false>{});
+    if (!a.full) {  // partial A windows (sharded tails below bit 12): runtime masks
+      if (c) return ksin ? L(SweepKernel<SA, NV, GF_FACT_C, true, false>{}) : L(SweepKernel<SA, NV, GF_FACT_C, false, false>{});
+      return ksin ? L(SweepKernel<SA, NV, GF_FACT_S, true, false>{}) : L(SweepKernel<SA, NV, GF_FACT_S, false, false>{});
+    }
+    if (c) return ksin ? L(SweepKernel<SA, NV, GF_FACT_C, true, true>{}) : L(SweepKernel<SA, NV, GF_FACT_C, false, true>{});
+    return ksin ? L(SweepKernel<SA, NV, GF_FACT_S, true, true>{}) : L(SweepKernel<SA, NV, GF_FACT_S, false, true>{});
   }
-  return c ? L(SweepKernel<SB, NV, GF_FACT_C, false>{}) : L(SweepKernel<SB, NV, GF_FACT_S, false>{});
+  if (a.full) return c ? L(SweepKernel<SB, NV, GF_FACT_C, false, true>{}) : L(SweepKernel<SB, NV, GF_FACT_S, false, true>{});
+  return c ? L(SweepKernel<SB, NV, GF_FACT_C, false, false>{}) : L(SweepKernel<SB, NV, GF_FACT_S, false, false>{});
 }
 
 // exact-mode instantiations (ascending qubit order, FMA-free): shapes A2X / B2
 template <int NV>
 int launch_exact(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
   auto L = [&](auto k) { return decltype(k)::launch(ctx, a, g); };
-  if (a.shape == SH_A2X)
-    return a.kind == 0 ? L(SweepKernel<SH_A2X, NV, GF_EXACT, true>{}) : L(SweepKernel<SH_A2X, NV, GF_EXACT, false>{});
-  return L(SweepKernel<SH_B2, NV, GF_EXACT, false>{});
+  if (a.shape == SH_A2X) {
+    if (!a.full)
+      return a.kind == 0 ? L(SweepKernel<SH_A2X, NV, GF_EXACT, true, false>{})
+                         : L(SweepKernel<SH_A2X, NV, GF_EXACT, false, false>{});
+    return a.kind == 0 ? L(SweepKernel<SH_A2X, NV, GF_EXACT, true, true>{})
+                       : L(SweepKernel<SH_A2X, NV, GF_EXACT, false, true>{});
+  }
+  return a.full ? L(SweepKernel<SH_B2, NV, GF_EXACT, false, true>{}) : L(SweepKernel<SH_B2, NV, GF_EXACT, false, false>{});
 }
 
 }  // namespace sweepk
