@@ -262,6 +262,16 @@ def load_peaks() -> dict:
     return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
+def kernel_label(kind: str) -> str:
+    """sweep kind (DeviceContext.prof_kind_name) -> the k_sweep instantiation it runs"""
+    vec, *mode, win = kind.split("_")
+    mode = mode[0] if mode else "plain"
+    nv = 1 if vec == "single" else 2
+    what = {"plain": "one layer's gates", "merged": "two layers' gates + the diagonal between them",
+            "bridge": "last forward + first backward layer, <C>, bra = C*ket"}[mode]
+    return f"k_sweep<SH_{win}2, NV={nv}, MODE={mode}> ({win} window, {what})"
+
+
 def load_traffic() -> dict:
     p = ROOT / "profiles" / "traffic.json"
     return json.loads(p.read_text()) if p.exists() else {}
@@ -433,7 +443,7 @@ def run_b200(args, rank: int, world: int, dist) -> None:
         "gpu_launches": launches,
         "roofline": {
             "bound": "hbm",
-            "kernel": "k_sweep<4,3,2> (bra/ket sweep)" if dom == "sweep2" else "k_sweep<5,2,1> (single-vector sweep)",
+            "kernel": kernel_label(dom),
             "achieved": achieved,
             "peak": peaks["hbm_gbs"],
             "peak_source": peaks["source"],

@@ -181,11 +181,21 @@ class DeviceContext:
     def prof_begin(self) -> None:
         call("qsb_prof_begin", self.handle)
 
+    PROF_KINDS = 12
+
+    @staticmethod
+    def prof_kind_name(k: int) -> str:
+        mode, nv, win = k // 4, (k // 2) % 2 + 1, "B" if k % 2 else "A"
+        return f"{'single' if nv == 1 else 'braket'}{['', '_merged', '_bridge'][mode]}_{win}"
+
     def prof_end(self) -> dict:
-        """{kind: (launches, total_ms, algorithmic_bytes)} for kinds 'sweep1', 'sweep2'."""
-        out = (C.c_double * 6)()
-        call("qsb_prof_end", self.handle, out, 2)
-        return {"sweep1": (out[0], out[1], out[2]), "sweep2": (out[3], out[4], out[5])}
+        """{kind: (launches, total_ms, algorithmic_bytes)} per sweep kind, e.g.
+        'single_A', 'braket_merged_B', 'braket_bridge_A' (kinds with no launch omitted)."""
+        nk = self.PROF_KINDS
+        out = (C.c_double * (3 * nk))()
+        call("qsb_prof_end", self.handle, out, nk)
+        return {self.prof_kind_name(k): (out[3 * k], out[3 * k + 1], out[3 * k + 2])
+                for k in range(nk) if out[3 * k] > 0}
 
     def timer_start(self) -> None:
         call("qsb_timer_start", self.handle)

@@ -180,8 +180,9 @@ int qsb_prof_begin(qsb_ctx* ctx) {
   return QSB_OK;
 }
 
-// out[3*k + 0..2] = launches, total ms, algorithmic bytes for kernel kind k
-// (k = 0: single-vector sweep, 1: bra/ket sweep); nkinds entries are written.
+// out[3*k + 0..2] = launches, total ms, algorithmic bytes for kernel kind k =
+// (mode * 2 + nv - 1) * 2 + (B window ? 1 : 0) (mode: 0 plain, 1 merged, 2 bridge);
+// nkinds entries are written.
 int qsb_prof_end(qsb_ctx* ctx, double* out, int nkinds) {
   if (!ctx || !out) return invalid("null argument");
   ctx->prof = false;

@@ -64,7 +64,8 @@ int sweep_family(int nv) {
 }
 
 // Fill the tile/phase part of SweepArgs for one sweep. Returns the number of gates.
-int build_shape(const SweepShape& sh, int n, int nv, bool exact, SweepArgs& a, int gates_before_phase[kMaxPhases]) {
+int build_shape(const SweepShape& sh, int n, int nv, bool exact, SweepArgs& a, int gates_before_phase[kMaxPhases],
+                const int* pass2 = nullptr, int gates_before_phase2[kMaxPhases] = nullptr, int* gates2 = nullptr) {
   int gl[kSweepT];
   for (int i = 0; i < kSweepT; ++i) gl[i] = sh.is_a ? i : (i < 3 ? i : sh.glo + i - 3);
   const int shape = pick_shape(exact, sh.is_a, sweep_family(nv));
@@ -144,6 +145,30 @@ int build_shape(const SweepShape& sh, int n, int nv, bool exact, SweepArgs& a, i
   if (a.full)
     for (int p = 0; p < np; ++p)
       if (a.ph[p].apply != shape_apply(shape, p)) return -1;  // planner and kernel must agree
+  if (pass2) {
+    // second pass of a merged sweep: qubits [pass2[0], pass2[1]], phases in reverse order
+    bool applied2[kSweepT] = {false};
+    int g2 = 0;
+    bool full2 = true;
+    for (int pp = 0; pp < np; ++pp) {
+      const int p = np - 1 - pp;
+      gates_before_phase2[p] = g2;
+      uint8_t apply = 0;
+      for (int b = 0; b < R; ++b) {
+        const int loc = ps[p].reg_l + b;
+        const int g = gl[loc];
+        if (ps[p].allow && !applied2[loc] && g >= pass2[0] && g <= pass2[1]) {
+          apply |= (uint8_t)(1u << b);
+          applied2[loc] = true;
+          ++g2;
+        }
+      }
+      a.apply2[p] = apply;
+      if (apply != shape_apply_rev(shape, p)) full2 = false;
+    }
+    *gates2 = g2;
+    a.full = a.full && full2;
+  }
   return gates;
 }
 
@@ -274,39 +299,50 @@ struct Runner {
     return QSB_OK;
   }
 
-  // algorithmic HBM bytes of one sweep: every amplitude read/written once,
-  // plus one table read (compact index or f64) per fused table use
-  double alg_bytes(int nv, uint32_t flags) const {
+  // algorithmic HBM bytes of one sweep: every amplitude read/written once, plus
+  // one read of the table (compact index or f64) when the sweep has table ops
+  double alg_bytes(int nv, int mode, uint32_t flags) const {
     const double N = (double)(1ull << n);
     const double tb = t ? (t->kind == 1 ? 1.0 : t->kind == 2 ? 2.0 : 8.0) : 0.0;
     double b = 0.0;
     if (nv == 1) {
       if (!(flags & SF_PLUS)) b += 16.0 * N;
       if (!(flags & SF_NO_STORE)) b += 16.0 * N;
-      if (flags & SF_PRE_PHASE) b += tb * N;
-      if (flags & SF_POST_EXPECT) b += tb * N;
     } else {
-      b += (flags & SF_BRA_FROM_KET) ? 16.0 * N : 32.0 * N;
+      b += (mode == SM_BRIDGE || (flags & SF_BRA_FROM_KET)) ? 16.0 * N : 32.0 * N;
       if (!(flags & SF_NO_STORE)) b += 32.0 * N;
-      if (flags & (SF_PRE_PHASE | SF_BRA_FROM_KET | SF_PRE_DINNER)) b += tb * N;
-      if (flags & SF_POST_DINNER) b += tb * N;
     }
+    if (flags & kTableOps) b += tb * N;
     return b;
   }
 
-  // launch one sweep; returns its index for partial lookup
+  // live-profiler kind (qsb_prof_end): ((mode * 2 + nv - 1) * 2 + is_b), 12 kinds
+  static int prof_kind(int nv, int mode, bool is_a) { return ((mode * 2 + nv - 1) * 2) + (is_a ? 0 : 1); }
+
+  static constexpr uint32_t kTableOps = SF_PRE_PHASE | SF_BRA_FROM_KET | SF_PRE_DINNER | SF_POST_EXPECT |
+                                        SF_POST_DINNER | SF_MID_PHASE | SF_MID_DINNER | SF_MID_EXPECT;
+
+  // one plain sweep (one gate pass) over window `sh`, gates on [sh.lo, sh.hi]
   int sweep(int nv, const SweepShape& sh, double2* v0, double2* v1, const Gate& g, uint32_t flags,
             const double2* lut, double pre_ang, double2 pre_extra, bool want_partials, int* idx_out) {
+    return sweep_any(nv, SM_PLAIN, sh, nullptr, v0, v1, g, g, flags, lut, pre_ang, pre_extra, want_partials, idx_out);
+  }
+
+  // general sweep: pass 1 gates g1 on [sh.lo, sh.hi]; merged / bridge sweeps add
+  // mid ops and pass 2 gates g2 on [pass2[0], pass2[1]] (phases in reverse order)
+  int sweep_any(int nv, int mode, const SweepShape& sh, const int* pass2, double2* v0, double2* v1, const Gate& g1,
+                const Gate& g2, uint32_t flags, const double2* lut, double pre_ang, double2 pre_extra,
+                bool want_partials, int* idx_out) {
     SweepArgs a;
     memset(&a, 0, sizeof(a));
-    int gbp[kMaxPhases];
-    const int gates = build_shape(sh, n, nv, exact, a, gbp);
+    int gbp[kMaxPhases], gbp2[kMaxPhases] = {0, 0, 0, 0}, gates2 = 0;
+    const int gates = build_shape(sh, n, nv, exact, a, gbp, mode != SM_PLAIN ? pass2 : nullptr, gbp2, &gates2);
     if (gates < 0) return invalid("internal: bad sweep layout");
+    a.mode = mode;
     a.v0 = v0;
     a.v1 = v1;
     set_table(a, t);
-    const bool table_ops = flags & (SF_PRE_PHASE | SF_BRA_FROM_KET | SF_PRE_DINNER | SF_POST_EXPECT | SF_POST_DINNER);
-    a.cmode = (t && t->kind != 0 && table_ops) ? ((!sh.is_a && t->kind == 1) ? 2 : 1) : 0;
+    a.cmode = (t && t->kind != 0 && (flags & kTableOps)) ? ((!sh.is_a && t->kind == 1) ? 2 : 1) : 0;
     if (!sh.is_a) {  // TMA boxes for the strided B tiles
       QSB_TRY(encode_b_tile_map(&a.tm0, v0, n, sh.glo));
       if (nv == 2) QSB_TRY(encode_b_tile_map(&a.tm1, v1, n, sh.glo));
@@ -315,13 +351,28 @@ struct Runner {
     a.lut = lut;
     a.pre_ang = pre_ang;
     a.pre_extra = pre_extra;
-    a.form = g.form;
-    a.ga = g.ga;
-    a.gb = g.gb;
+    a.form = g1.form;
+    a.ga = g1.ga;
+    a.gb = g1.gb;
     a.plus_amp = plus_amp > 0.0 ? plus_amp : 1.0 / sqrt((double)(1ull << n));
-    for (int p = 0; p < kMaxPhases; ++p) a.xs_w[p] = ipow(g.sigma * g.sigma, gbp[p]);
-    a.post_scale = ipow(g.sigma, gates);
-    if (!exact && gates > 0) flags |= SF_POST_SCALE;
+    const double s1 = g1.sigma * g1.sigma;
+    for (int p = 0; p < kMaxPhases; ++p) a.xs_w[p] = ipow(s1, gbp[p]);
+    a.w0 = a.w1 = 1.0;
+    if (mode != SM_PLAIN) {
+      // pass-1 scale is still pending at the mid ops and throughout pass 2
+      const double m = ipow(s1, gates);
+      a.w0 = a.w1 = m;
+      a.form2 = g2.form;
+      a.ga2 = g2.ga;
+      a.gb2 = g2.gb;
+      for (int p = 0; p < kMaxPhases; ++p) a.xs_w2[p] = m * ipow(g2.sigma * g2.sigma, gbp2[p]);
+      a.post_scale = ipow(g1.sigma, gates) * ipow(g2.sigma, gates2);
+      if (gates + gates2 > 0) flags |= SF_POST_SCALE;
+    } else {
+      a.form2 = g1.form;
+      a.post_scale = ipow(g1.sigma, gates);
+      if (!exact && gates > 0) flags |= SF_POST_SCALE;
+    }
     a.flags = flags;
     const int idx = nsweeps_launched++;
     a.partials = want_partials ? partials + (uint64_t)idx * kSlots * maxgrid : nullptr;
@@ -331,7 +382,7 @@ struct Runner {
     QSB_TRY(launch_sweep(ctx, nv, exact, a, &grid));
     if (ctx->prof) {
       QSB_TRY(prof_mark(ctx, &e1));
-      ctx->prof_recs.push_back({e0, e1, nv - 1, alg_bytes(nv, flags)});
+      ctx->prof_recs.push_back({e0, e1, prof_kind(nv, mode, sh.is_a), alg_bytes(nv, mode, flags)});
     }
     grids.push_back(grid);
     if (idx_out) *idx_out = idx;
@@ -386,6 +437,181 @@ int forward_fused(Runner& R, double2* amps, int p, const double* gammas, const d
   return QSB_OK;
 }
 
+// ------------------------------------------------------------------ the window chain
+// Every layer (forward or backward) applies its Rx gates window by window.  Layer
+// directions alternate (A, B1, .., Bk | Bk, .., B1, A | ...; backward layer i runs
+// opposite to forward layer i), so consecutive layers meet on the same window and
+// the two visits fuse into ONE merged sweep whose mid ops are the diagonal work
+// between the layers: a layer of p forward + p backward costs 2p(K-1)+1 HBM passes
+// instead of 2pK (K = windows per layer; n=30: K=3, 25 passes instead of 36).
+struct Visit {
+  bool bwd;
+  int layer;
+  int win;
+  int lo, hi;
+};
+
+// slot contribution of a launched sweep: kind 0 = value, 1 = d_gamma[layer], 2 = d_beta[layer]
+struct Contrib {
+  int sweep, slot, kind, layer;
+};
+
+// QSB_NO_MERGE=1 runs every visit as its own sweep (A/B comparisons, tests)
+bool merge_enabled() {
+  const char* e = getenv("QSB_NO_MERGE");
+  return !(e && atoi(e));
+}
+
+std::vector<Visit> chain_visits(int n, const std::vector<SweepShape>& wins, int p, bool fwd, bool bwd) {
+  const int K = (int)wins.size();
+  std::vector<Visit> out;
+  auto gate_mask = [&](int w) -> uint64_t {
+    const int lo = wins[w].is_a ? 0 : wins[w].glo;
+    const int hi = wins[w].is_a ? std::min(kSweepT, n) - 1 : wins[w].glo + 8;
+    return ((hi >= 63 ? ~0ull : ((1ull << (hi + 1)) - 1)) & ~((1ull << lo) - 1));
+  };
+  auto layer = [&](bool b, int i) {
+    const bool ascending = b ? (i % 2 == 1) : (i % 2 == 0);
+    uint64_t covered = 0;
+    for (int k = 0; k < K; ++k) {
+      const int w = ascending ? k : K - 1 - k;
+      const uint64_t m = gate_mask(w) & ~covered;
+      covered |= m;
+      if (!m) continue;
+      out.push_back({b, i, w, __builtin_ctzll(m), 63 - __builtin_clzll(m)});
+    }
+  };
+  if (fwd)
+    for (int i = 0; i < p; ++i) layer(false, i);
+  if (bwd)
+    for (int i = p - 1; i >= 0; --i) layer(true, i);
+  return out;
+}
+
+// Runs forward layers 0..p-1 (fwd) and/or the adjoint walk p-1..0 (bwd) as one chain
+// of sweeps.  Contributions to <C> / d_gamma / d_beta are recorded in `contribs`.
+int run_chain(Runner& R, double2* ket, double2* bra, int p, const double* gammas, const double* betas, bool fwd,
+              bool from_plus, bool want_value, bool bwd, std::vector<Contrib>& contribs) {
+  const int n = R.n;
+  const std::vector<SweepShape>& wins = R.shapes;
+  const std::vector<Visit> vis = chain_visits(n, wins, p, fwd, bwd);
+  const int M = (int)vis.size();
+  const bool merge = merge_enabled() && wins.size() >= 2;
+  const double2 one = make_double2(1.0, 0.0);
+  const uint64_t nvals = R.t->kind != 0 ? (uint64_t)R.t->nvals : 0;
+  auto fwd_lut = [&](int i) { return R.t->kind != 0 ? R.t->d_lut + (size_t)i * nvals : nullptr; };
+  auto inv_lut = [&](int i) { return R.t->kind != 0 ? R.t->d_lut + (size_t)(p + i) * nvals : nullptr; };
+  auto gate_of = [&](const Visit& v) { return make_gate((v.bwd ? 2.0 : -2.0) * betas[v.layer], false); };
+  auto win_of = [&](const Visit& v) {
+    SweepShape sh = wins[v.win];
+    sh.lo = v.lo;
+    sh.hi = v.hi;
+    return sh;
+  };
+  // boundary kinds between visit u and u+1: 0 none (same layer), 1 fwd->fwd, 2 fwd->bwd, 3 bwd->bwd
+  auto boundary = [&](int u) {
+    const Visit &a = vis[u], &b = vis[u + 1];
+    if (a.bwd == b.bwd && a.layer == b.layer) return 0;
+    if (!a.bwd && !b.bwd) return 1;
+    if (!a.bwd && b.bwd) return 2;
+    return 3;
+  };
+
+  for (int u = 0; u < M;) {
+    const Visit& v = vis[u];
+    const bool pair = merge && u + 1 < M && vis[u + 1].win == v.win && boundary(u) != 0;
+    int idx = -1;
+    if (pair) {
+      const Visit& w = vis[u + 1];
+      const int kind = boundary(u);
+      const int pass2[2] = {w.lo, w.hi};
+      uint32_t f = 0;
+      int mode = SM_MERGED, nv = v.bwd ? 2 : 1;
+      const double2* lut = nullptr;
+      double ang = 0.0;
+      if (kind == 1) {  // forward layer i -> i+1: phase exp(-i g_{i+1} C)
+        f |= SF_MID_PHASE;
+        lut = fwd_lut(w.layer);
+        ang = -gammas[w.layer];
+      } else if (kind == 2) {  // last forward layer -> first backward layer
+        mode = SM_BRIDGE;
+        nv = 2;
+        if (want_value) f |= SF_MID_EXPECT;
+        f |= SF_XSUM2;
+      } else {  // backward layer i -> i-1: <bra|C|ket>, then the inverse phase exp(+i g_i C)
+        f |= SF_XSUM | SF_MID_DINNER | SF_MID_PHASE | SF_XSUM2;
+        lut = inv_lut(v.layer);
+        ang = gammas[v.layer];
+      }
+      QSB_TRY(R.sweep_any(nv, mode, win_of(v), pass2, ket, bra, gate_of(v), gate_of(w), f, lut, ang, one, true, &idx));
+      if (kind == 2 && want_value) contribs.push_back({idx, 0, 0, 0});
+      if (v.bwd) contribs.push_back({idx, 2, 2, v.layer});
+      if (kind == 3) contribs.push_back({idx, 1, 1, v.layer});
+      if (w.bwd) contribs.push_back({idx, 3, 2, w.layer});
+      u += 2;
+      continue;
+    }
+    // single visit: pre ops from the boundary before it, post ops from the one after
+    uint32_t f = 0;
+    const double2* lut = nullptr;
+    double ang = 0.0;
+    int dinner_pre = -1;
+    const int before = u == 0 ? -1 : boundary(u - 1);
+    if (u == 0) {
+      if (fwd) {
+        if (from_plus) f |= SF_PLUS;
+        f |= SF_PRE_PHASE;
+        lut = fwd_lut(0);
+        ang = -gammas[0];
+      } else {
+        f |= SF_BRA_FROM_KET;
+      }
+    } else if (before == 1) {
+      f |= SF_PRE_PHASE;
+      lut = fwd_lut(v.layer);
+      ang = -gammas[v.layer];
+    } else if (before == 2) {
+      f |= SF_BRA_FROM_KET;
+    } else if (before == 3) {
+      f |= SF_PRE_DINNER | SF_PRE_PHASE;
+      dinner_pre = vis[u - 1].layer;
+      lut = inv_lut(dinner_pre);
+      ang = gammas[dinner_pre];
+    }
+    bool post_expect = false, post_dinner = false;
+    if (u == M - 1) {
+      if (v.bwd) post_dinner = true;
+      else post_expect = want_value;
+    } else if (boundary(u) == 2) {
+      post_expect = want_value;
+    }
+    if (post_expect) f |= SF_POST_EXPECT;
+    if (post_dinner) f |= SF_POST_DINNER | SF_NO_STORE;
+    if (v.bwd) f |= SF_XSUM;
+    QSB_TRY(R.sweep(v.bwd ? 2 : 1, win_of(v), ket, bra, gate_of(v), f, lut, ang, one, true, &idx));
+    if (post_expect) contribs.push_back({idx, 0, 0, 0});
+    if (post_dinner) contribs.push_back({idx, 0, 1, v.layer});
+    if (dinner_pre >= 0) contribs.push_back({idx, 1, 1, dinner_pre});
+    if (v.bwd) contribs.push_back({idx, 2, 2, v.layer});
+    ++u;
+  }
+  return QSB_OK;
+}
+
+// reduce the recorded contributions (fixed order) into value / d_gammas / d_betas
+void collect(const Runner& R, const std::vector<double>& h, const std::vector<Contrib>& cs, double* value,
+             double* dg, double* db, int p) {
+  if (value) *value = 0.0;
+  for (int i = 0; i < p && dg; ++i) dg[i] = 0.0;
+  for (int i = 0; i < p && db; ++i) db[i] = 0.0;
+  for (const Contrib& c : cs) {
+    const double x = Runner::slot_sum(h, R.maxgrid, R.grids, c.sweep, c.slot);
+    if (c.kind == 0 && value) *value += x;
+    else if (c.kind == 1 && dg) dg[c.layer] += 2.0 * x;
+    else if (c.kind == 2 && db) db[c.layer] += -2.0 * x;
+  }
+}
+
 int upper_sweeps(int n, int p) { return 2 * p * (int)plan_sweeps(n).size() + 4; }
 
 }  // namespace
@@ -431,7 +657,7 @@ int qsb_layer_sweeps(qsb_ctx* ctx, qsb_table* t, double* v0, double* v1, int nv,
   }
   std::vector<double> h;
   QSB_TRY(R.fetch(h));
-  for (int k = 0; k < kSlots; ++k) {
+  for (int k = 0; k < 3; ++k) {  // slot 3 (second-pass xsum) is unused by plain sweeps
     double acc = 0.0;
     for (int sw = 0; sw < ns; ++sw) acc += Runner::slot_sum(h, R.maxgrid, R.grids, sw, k);
     sums[k] = acc;
@@ -483,18 +709,18 @@ int qsb_simulate_expect(qsb_ctx* ctx, qsb_table* t, double* amps, int p, const d
     extras.push_back(make_double2(1.0, 0.0));
   }
   QSB_TRY(prepare_luts(t, scales, extras, exact));
-  const bool fused_e = expect_out && !exact;
-  int esweep = -1;
-  QSB_TRY(forward_fused(R, a, p, gammas, betas, flags, fused_e ? &esweep : nullptr, 0));
-  if (expect_out) {
-    if (fused_e) {
+  if (!exact) {
+    std::vector<Contrib> cs;
+    QSB_TRY(run_chain(R, a, nullptr, p, gammas, betas, true, flags & QSB_FROM_PLUS, expect_out != nullptr, false, cs));
+    if (expect_out) {
       std::vector<double> h;
       QSB_TRY(R.fetch(h));
-      *expect_out = Runner::slot_sum(h, R.maxgrid, R.grids, esweep, 0);
-    } else {
-      QSB_TRY(expectation_exact(ctx, t->values, a, t->len, expect_out));
+      collect(R, h, cs, expect_out, nullptr, nullptr, p);
     }
+    return QSB_OK;
   }
+  QSB_TRY(forward_fused(R, a, p, gammas, betas, flags, nullptr, 0));
+  if (expect_out) QSB_TRY(expectation_exact(ctx, t->values, a, t->len, expect_out));
   return QSB_OK;
 }
 
@@ -563,51 +789,12 @@ int qsb_value_and_grad(qsb_ctx* ctx, qsb_table* t, double* ket_, double* bra_, i
   }
   QSB_TRY(prepare_luts(t, scales, extras, false));
 
-  int esweep = -1;
-  if (!skip_forward) QSB_TRY(forward_fused(R, ket, p, gammas, betas, QSB_FROM_PLUS, value ? &esweep : nullptr, 0));
-
-  const int ns = (int)R.shapes.size();
-  std::vector<std::vector<int>> xs_sweeps(p);
-  std::vector<int> dg_sweep(p, -1);
-  for (int i = p - 1; i >= 0; --i) {
-    const Gate g = make_gate(2.0 * betas[i], false);
-    for (int s = 0; s < ns; ++s) {
-      uint32_t f = SF_XSUM;
-      const double2* lut = nullptr;
-      double pre_ang = 0.0;
-      if (s == 0) {
-        if (i == p - 1) {
-          f |= SF_BRA_FROM_KET;
-        } else {
-          // close layer i+1: <bra|C|ket> then its inverse phase exp(+i g_{i+1} C)
-          f |= SF_PRE_DINNER | SF_PRE_PHASE;
-          pre_ang = gammas[i + 1];
-          if (t->kind != 0) lut = t->d_lut + (size_t)(p + i + 1) * t->nvals;
-        }
-      }
-      const bool last = (i == 0) && (s == ns - 1);
-      if (last) f |= SF_POST_DINNER | SF_NO_STORE;
-      int idx;
-      QSB_TRY(R.sweep(2, R.shapes[s], ket, bra, g, f, lut, pre_ang, make_double2(1.0, 0.0), true, &idx));
-      xs_sweeps[i].push_back(idx);
-      if (s == 0 && i < p - 1) dg_sweep[i + 1] = idx;
-      if (last) dg_sweep[0] = idx;
-    }
-  }
+  std::vector<Contrib> cs;
+  QSB_TRY(run_chain(R, ket, bra, p, gammas, betas, !skip_forward, true, value != nullptr && !skip_forward, true, cs));
   std::vector<double> h;
   QSB_TRY(R.fetch(h));
-  for (int i = 0; i < p; ++i) {
-    double xs = 0.0;
-    for (int sw : xs_sweeps[i]) xs += Runner::slot_sum(h, R.maxgrid, R.grids, sw, 2);
-    d_betas[i] = -2.0 * xs;
-    // layer 0's contraction comes from the last sweep's post op (slot 0), the
-    // others from the next layer group's first sweep (slot 1)
-    d_gammas[i] = 2.0 * Runner::slot_sum(h, R.maxgrid, R.grids, dg_sweep[i], i == 0 ? 0 : 1);
-  }
-  if (value) {
-    if (esweep >= 0) *value = Runner::slot_sum(h, R.maxgrid, R.grids, esweep, 0);
-    else *value = NAN;  // skip_forward: caller already has it
-  }
+  collect(R, h, cs, value, d_gammas, d_betas, p);
+  if (value && skip_forward) *value = NAN;  // caller already has it
   return QSB_OK;
 }
 

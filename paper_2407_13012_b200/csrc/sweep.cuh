@@ -9,7 +9,9 @@ namespace qsb {
 
 constexpr int kSweepT = 12;        // tile = 2^12 amplitudes per vector
 constexpr int kMaxPhases = 4;
-constexpr int kSlots = 3;          // partial-sum slots: 0 expectation / post diag inner, 1 pre diag inner, 2 xsum
+// partial-sum slots: 0 expectation / post diag inner (mid expectation in a bridge),
+// 1 pre (or mid) diag inner, 2 xsum of the first gate pass, 3 xsum of the second
+constexpr int kSlots = 4;
 
 enum SweepFlags : uint32_t {
   SF_PLUS = 1u << 0,         // input is |+> (not loaded)
@@ -21,6 +23,22 @@ enum SweepFlags : uint32_t {
   SF_POST_DINNER = 1u << 6,  // NV=2: slot0 += T*Im(conj(bra) ket) after gates and post scale
   SF_NO_STORE = 1u << 7,
   SF_POST_SCALE = 1u << 8,   // multiply by the real post_scale after the gates
+  // merged sweeps (two gate passes over the same window, see SweepMode)
+  SF_MID_PHASE = 1u << 9,    // between the passes: multiply by the phase (LUT / pre_ang)
+  SF_MID_DINNER = 1u << 10,  // NV=2 merged: slot1 += T*Im(conj(bra) ket) between the passes
+  SF_MID_EXPECT = 1u << 11,  // bridge: slot0 += T*|ket|^2 between the passes
+  SF_XSUM2 = 1u << 12,       // NV=2: slot3 += xsum over the second pass's qubits
+};
+
+// A merged sweep applies two layers' gates to one window per HBM pass.  The chain
+// of windows visited by a layer alternates direction (A,B1,B2 | B2,B1,A | ...), so
+// consecutive layers meet on the same window; the diagonal operators between them
+// (phase, <bra|C|ket>, bra = C*ket, <C>) are elementwise and run between the passes.
+enum SweepMode : int {
+  SM_PLAIN = 0,   // one gate pass (+ pre / post ops)
+  SM_MERGED = 1,  // pass 1 (layer i) -> mid ops -> pass 2 (layer i+-1), same vectors
+  SM_BRIDGE = 2,  // NV=2: pass 1 on the ket only (last forward layer) -> <C>, bra = C*ket
+                  // -> pass 2 on both (first backward layer)
 };
 
 // gate forms: new0 = a*t - i*b*u, new1 = -i*b*t + a*u  (times an external real scale)
@@ -53,6 +71,14 @@ struct SweepArgs {
   double ga, gb;          // gate coefficients (see GateForm)
   double plus_amp;        // 1/sqrt(N)
   double xs_w[kMaxPhases];
+  // merged sweeps: second pass gates (same form family as `form2`), its per-phase
+  // xsum weights and gate masks, and end-of-sweep weights of slots 0 / 1
+  double ga2, gb2;
+  double xs_w2[kMaxPhases];
+  double w0, w1;
+  uint8_t apply2[kMaxPhases];
+  int form2;
+  int mode;
   double* partials;       // [kSlots][gridDim.x]
   uint64_t ntiles;
   uint32_t flags;
@@ -131,6 +157,8 @@ __host__ __device__ constexpr PhaseSpec shape_phase(int sh, int p) {
 
 // Gate mask of phase p when the whole window is targeted: register bits that are a
 // register bit for the first time (and the phase is allowed to apply gates).
+// shape_apply_rev: the same for the reversed phase order (second pass of a merged
+// sweep runs phases NP-1 .. 0).
 __host__ __device__ constexpr uint32_t shape_apply(int sh, int p) {
   uint32_t m = 0;
   const PhaseSpec P = shape_phase(sh, p);
@@ -139,6 +167,22 @@ __host__ __device__ constexpr uint32_t shape_apply(int sh, int p) {
     const int loc = P.reg_l + b;
     bool seen = false;
     for (int q = 0; q < p; ++q) {
+      const PhaseSpec Q = shape_phase(sh, q);
+      if (Q.allow && loc >= Q.reg_l && loc < Q.reg_l + shape_r(sh)) seen = true;
+    }
+    if (!seen) m |= 1u << b;
+  }
+  return m;
+}
+
+__host__ __device__ constexpr uint32_t shape_apply_rev(int sh, int p) {
+  uint32_t m = 0;
+  const PhaseSpec P = shape_phase(sh, p);
+  if (!P.allow) return 0;
+  for (int b = 0; b < shape_r(sh); ++b) {
+    const int loc = P.reg_l + b;
+    bool seen = false;
+    for (int q = shape_np(sh) - 1; q > p; --q) {
       const PhaseSpec Q = shape_phase(sh, q);
       if (Q.allow && loc >= Q.reg_l && loc < Q.reg_l + shape_r(sh)) seen = true;
     }

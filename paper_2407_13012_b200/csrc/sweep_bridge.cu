@@ -1,0 +1,10 @@
+// Bridge-sweep instantiations: the last forward layer's window pass on the ket, <C>,
+// bra = C*ket, then the first backward layer's pass on both (NV=2).
+#include "sweep_impl.cuh"
+
+namespace qsb {
+int launch_sweep_bridge(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
+  if (a.form == GF_FACT_C) return sweepk::launch_merged_f1<2, SM_BRIDGE, GF_FACT_C>(ctx, a, g);
+  return sweepk::launch_merged_f1<2, SM_BRIDGE, GF_FACT_S>(ctx, a, g);
+}
+}  // namespace qsb

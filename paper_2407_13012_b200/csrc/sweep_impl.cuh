@@ -27,6 +27,8 @@
 // rides the A-tile TMA), bra = C*ket, <bra|C|ket>, sum_j <bra|X_j|ket> (before each
 // phase's gates) and <psi|C|psi>.
 #pragma once
+#include <type_traits>
+
 #include "sweep.cuh"
 
 namespace qsb {
@@ -141,18 +143,60 @@ __device__ __forceinline__ void butterfly(double2& t, double2& u, double ga, dou
   }
 }
 
+// gates on the register bits in `apply`, for the first NVA vectors
+template <int FORM, int NVA, int NV, int NR, int R>
+__device__ __forceinline__ void gate_bits(double2 (&v)[NV][NR], uint32_t apply, double ga, double gb) {
+#pragma unroll
+  for (int b = 0; b < R; ++b) {
+    if (apply & (1u << b)) {
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        if (j & (1 << b)) continue;
+        const int k2 = j | (1 << b);
+#pragma unroll
+        for (int q = 0; q < NVA; ++q) butterfly<FORM>(v[q][j], v[q][k2], ga, gb);
+      }
+    }
+  }
+}
+
+// Im sum_{b in apply} <bra|X_b|ket> over this thread's register pairs (NV == 2)
+template <int NR, int R>
+__device__ __forceinline__ double xsum_bits(const double2 (&v)[2][NR], uint32_t apply) {
+  double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
+#pragma unroll
+  for (int b = 0; b < R; ++b) {
+    if (apply & (1u << b)) {
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        if (j & (1 << b)) continue;
+        const int k2 = j | (1 << b);
+        x0 = fma(v[1][j].x, v[0][k2].y, x0);
+        x1 = fma(-v[1][j].y, v[0][k2].x, x1);
+        x2 = fma(v[1][k2].x, v[0][j].y, x2);
+        x3 = fma(-v[1][k2].y, v[0][j].x, x3);
+      }
+    }
+  }
+  return (x0 + x1) + (x2 + x3);
+}
+
 // ------------------------------------------------------------------ kernel
 // SH: shape, NV: vectors (1 or 2), FORM: gate arithmetic, KSIN: f64 table +
 // device sincos (else compact index + LUT), FULL: every window position is a
-// target (gate masks fixed at compile time by the shape).
-template <int SH, int NV, int FORM, bool KSIN, bool FULL>
+// target (gate masks fixed at compile time by the shape), MODE: SweepMode,
+// FORM2: gate arithmetic of the second pass (merged / bridge sweeps).
+template <int SH, int NV, int FORM, bool KSIN, bool FULL, int MODE, int FORM2>
 __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_constant__ SweepArgs a) {
   constexpr int R = shape_r(SH), W = shape_w(SH), NP = shape_np(SH);
   constexpr bool IS_A = shape_is_a(SH);
   constexpr bool EXACT = FORM == GF_EXACT;
   constexpr int NT = 32 << W;
   constexpr int NR = 1 << R;
+  constexpr int NVA = MODE == SM_BRIDGE ? 1 : NV;  // vectors of the pre ops and the first pass
   static_assert(5 + W + R == kSweepT, "tile size");
+  static_assert(MODE == SM_PLAIN || !EXACT, "merged sweeps are fast-mode only");
+  static_assert(MODE != SM_BRIDGE || NV == 2, "a bridge sweep produces the bra");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(smem_raw);
   const uint32_t cring_s = ring_s + kRing * kSlotBytes;
@@ -172,7 +216,7 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
     for (int s = 0; s < kRing; ++s) mbar_init(bar_s + 8 * s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (!KSIN && a.kind == 1 && (flags & SF_PRE_PHASE)) {  // u8 LUT in smem
+  if (!KSIN && a.kind == 1 && (flags & (SF_PRE_PHASE | SF_MID_PHASE))) {  // u8 LUT in smem
     for (int i = threadIdx.x; i < a.nlut; i += NT) slut[i] = a.lut[i];
   }
   __syncthreads();
@@ -189,7 +233,8 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
     const uint64_t tile = blockIdx.x + k * gridDim.x;
     const uint32_t slot = (uint32_t)(s % kRing);
     const uint32_t bar = bar_s + 8 * slot;
-    const bool vec = !((q == 0 && (flags & SF_PLUS)) || (q == 1 && (flags & SF_BRA_FROM_KET)));
+    const bool vec = !((q == 0 && (flags & SF_PLUS)) ||
+                       (q == 1 && (MODE == SM_BRIDGE || (flags & SF_BRA_FROM_KET))));
     const bool cid = cmode != 0 && (s % NV) == 0;
     const uint32_t bytes = (vec ? kSlotBytes : 0u) + (cid ? cbytes : 0u);
     if (bytes == 0) {
@@ -221,9 +266,8 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
   };
   auto wait_seq = [&](uint64_t s) { mbar_wait(bar_s + 8 * (uint32_t)(s % kRing), (uint32_t)((s / kRing) & 1)); };
 
-  double acc0 = 0.0, acc0b = 0.0, acc1 = 0.0, acc1b = 0.0, acc2 = 0.0;
+  double acc0 = 0.0, acc0b = 0.0, acc1 = 0.0, acc1b = 0.0, acc2 = 0.0, acc3 = 0.0;
   double2 v[NV][NR];
-
 
   issue(0);
   issue(1);
@@ -255,8 +299,10 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
       const uint32_t b_addr = ring_s + (uint32_t)((2 * k) % kRing) * kSlotBytes;
       xs_addr = ring_s + (uint32_t)((2 * k + 1) % kRing) * kSlotBytes;
       const uint32_t pb = b_addr + lb * 16u;
+      if constexpr (MODE != SM_BRIDGE) {
 #pragma unroll
-      for (int j = 0; j < NR; ++j) v[1][j] = lds(pb + (((uint32_t)j << P0.reg_l) * 16u));
+        for (int j = 0; j < NR; ++j) v[1][j] = lds(pb + (((uint32_t)j << P0.reg_l) * 16u));
+      }
       fence_proxy_async();
       __syncthreads();
       issue(2 * k + 3);  // ket of the next tile into the bra slot just read
@@ -265,51 +311,7 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
       for (int j = 0; j < NR; ++j) v[0][j] = lds(p0 + (((uint32_t)j << P0.reg_l) * 16u));
     }
 
-    // ---------------------------------------------------------------- pre ops
-    // table-kind dispatch hoisted out of the unrolled loops (tv: value / phase views)
-    auto pre_ops = [&](auto tv) {
-      const uint64_t g0 = base + gofs<IS_A>(lb, glo);
-      if constexpr (NV == 2) {
-        if (flags & SF_BRA_FROM_KET) {
-#pragma unroll
-          for (int j = 0; j < NR; ++j) {
-            const double t = tv.val(lb | ((uint32_t)j << P0.reg_l), g0 + gofs<IS_A>((uint32_t)j << P0.reg_l, glo));
-            v[1][j] = make_double2(t * v[0][j].x, t * v[0][j].y);
-          }
-        }
-        if (flags & SF_PRE_DINNER) {
-#pragma unroll
-          for (int j = 0; j < NR; ++j) {
-            const double t = tv.val(lb | ((uint32_t)j << P0.reg_l), g0 + gofs<IS_A>((uint32_t)j << P0.reg_l, glo));
-            const double d = v[1][j].x * v[0][j].y - v[1][j].y * v[0][j].x;
-            if (j & 1) acc1b = fma(t, d, acc1b);
-            else acc1 = fma(t, d, acc1);
-          }
-        }
-      }
-      if (flags & SF_PRE_PHASE) {
-#pragma unroll
-        for (int j = 0; j < NR; ++j) {
-          const double2 f = tv.phase(lb | ((uint32_t)j << P0.reg_l), g0 + gofs<IS_A>((uint32_t)j << P0.reg_l, glo));
-#pragma unroll
-          for (int q = 0; q < NV; ++q) v[q][j] = cmul<EXACT>(v[q][j], f);
-        }
-      }
-    };
-    // post ops: <psi|C|psi> (NV=1) or <bra|C|ket> (NV=2) after the gates, in the last map
-    constexpr int RL = shape_phase(SH, NP - 1).reg_l;
-    auto post_ops = [&](auto tv, uint32_t lbl) {
-      const uint64_t g1 = base + gofs<IS_A>(lbl, glo);
-#pragma unroll
-      for (int j = 0; j < NR; ++j) {
-        const double t = tv.val(lbl | ((uint32_t)j << RL), g1 + gofs<IS_A>((uint32_t)j << RL, glo));
-        double d;
-        if constexpr (NV == 1) d = fma(v[0][j].x, v[0][j].x, v[0][j].y * v[0][j].y);
-        else d = v[1][j].x * v[0][j].y - v[1][j].y * v[0][j].x;  // slot 0: PRE_DINNER may use slot 1
-        if (j & 1) acc0b = fma(t, d, acc0b);
-        else acc0 = fma(t, d, acc0);
-      }
-    };
+    // ---------------------------------------------------------------- table views
     struct TvF64 {  // f64 table from HBM, device sincos
       const SweepArgs& a;
       __device__ double val(uint32_t, uint64_t g) const { return a.table[g]; }
@@ -343,6 +345,7 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
       __device__ double val(uint32_t l, uint64_t) const { return a.vmin + (double)cs[at(l)]; }
       __device__ double2 phase(uint32_t l, uint64_t) const { return slut[cs[at(l)]]; }
     };
+    // table-kind dispatch hoisted out of the unrolled loops (tv: value / phase views)
     auto with_table = [&](auto&& fn) {
       if constexpr (KSIN) {
         fn(TvF64{a});
@@ -353,67 +356,121 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
         else fn(TvF64{a});
       }
     };
-    if (flags & (SF_PRE_PHASE | SF_BRA_FROM_KET | SF_PRE_DINNER)) with_table([&](auto tv) { pre_ops(tv); });
 
-    // ---------------------------------------------------------------- phases
+    // ---------------------------------------------------------------- pre ops
+    if constexpr (MODE == SM_PLAIN) {
+      auto pre_ops = [&](auto tv) {
+        const uint64_t g0 = base + gofs<IS_A>(lb, glo);
+        if constexpr (NV == 2) {
+          if (flags & SF_BRA_FROM_KET) {
 #pragma unroll
-    for (int p = 0; p < NP; ++p) {
-      const PhaseSpec P = shape_phase(SH, p);
-      if (p > 0) {
-        // exchange through this tile's slot (swizzled), one vector at a time
-        const PhaseSpec Q = shape_phase(SH, p - 1);
-        const uint32_t nlb = lbase<W>(P, lane, warp);
-        const uint32_t so = swz(lb) * 16u, sn = swz(nlb) * 16u;
-#pragma unroll
-        for (int q = 0; q < NV; ++q) {
-          __syncthreads();
-#pragma unroll
-          for (int j = 0; j < NR; ++j) sts(xs_addr + (so ^ (swz((uint32_t)j << Q.reg_l) * 16u)), v[q][j]);
-          __syncthreads();
-#pragma unroll
-          for (int j = 0; j < NR; ++j) v[q][j] = lds(xs_addr + (sn ^ (swz((uint32_t)j << P.reg_l) * 16u)));
-        }
-        lb = nlb;
-      }
-      // FULL: compile-time gate mask (no branches around the register tile)
-      const uint32_t apply = FULL ? shape_apply(SH, p) : a.ph[p].apply;
-      if constexpr (NV == 2) {
-        // sum_j <bra|X_j|ket> for this phase's qubits, before any of its gates
-        // (X_j commutes with every Rx): one scale factor xs_w[p] covers them
-        if (flags & SF_XSUM) {
-          double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
-#pragma unroll
-          for (int b = 0; b < R; ++b) {
-            if (apply & (1u << b)) {
-#pragma unroll
-              for (int j = 0; j < NR; ++j) {
-                if (j & (1 << b)) continue;
-                const int k2 = j | (1 << b);
-                x0 = fma(v[1][j].x, v[0][k2].y, x0);
-                x1 = fma(-v[1][j].y, v[0][k2].x, x1);
-                x2 = fma(v[1][k2].x, v[0][j].y, x2);
-                x3 = fma(-v[1][k2].y, v[0][j].x, x3);
-              }
+            for (int j = 0; j < NR; ++j) {
+              const double t = tv.val(lb | ((uint32_t)j << P0.reg_l), g0 + gofs<IS_A>((uint32_t)j << P0.reg_l, glo));
+              v[1][j] = make_double2(t * v[0][j].x, t * v[0][j].y);
             }
           }
-          acc2 = fma(a.xs_w[p], (x0 + x1) + (x2 + x3), acc2);
-        }
-      }
+          if (flags & SF_PRE_DINNER) {
 #pragma unroll
-      for (int b = 0; b < R; ++b) {
-        if (apply & (1u << b)) {
-#pragma unroll
-          for (int j = 0; j < NR; ++j) {
-            if (j & (1 << b)) continue;
-            const int k2 = j | (1 << b);
-#pragma unroll
-            for (int q = 0; q < NV; ++q) butterfly<FORM>(v[q][j], v[q][k2], a.ga, a.gb);
+            for (int j = 0; j < NR; ++j) {
+              const double t = tv.val(lb | ((uint32_t)j << P0.reg_l), g0 + gofs<IS_A>((uint32_t)j << P0.reg_l, glo));
+              const double d = v[1][j].x * v[0][j].y - v[1][j].y * v[0][j].x;
+              if (j & 1) acc1b = fma(t, d, acc1b);
+              else acc1 = fma(t, d, acc1);
+            }
           }
         }
+        if (flags & SF_PRE_PHASE) {
+#pragma unroll
+          for (int j = 0; j < NR; ++j) {
+            const double2 f = tv.phase(lb | ((uint32_t)j << P0.reg_l), g0 + gofs<IS_A>((uint32_t)j << P0.reg_l, glo));
+#pragma unroll
+            for (int q = 0; q < NV; ++q) v[q][j] = cmul<EXACT>(v[q][j], f);
+          }
+        }
+      };
+      if (flags & (SF_PRE_PHASE | SF_BRA_FROM_KET | SF_PRE_DINNER)) with_table([&](auto tv) { pre_ops(tv); });
+    }  // merged sweeps start and end mid-layer: no pre / post ops
+
+    // exchange the register tile from phase map Q to phase map P through this tile's
+    // slot (swizzled), one vector at a time
+    auto exchange = [&](const PhaseSpec Q, const PhaseSpec P, auto nvx) {
+      const uint32_t nlb = lbase<W>(P, lane, warp);
+      const uint32_t so = swz(lb) * 16u, sn = swz(nlb) * 16u;
+#pragma unroll
+      for (int q = 0; q < decltype(nvx)::value; ++q) {
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < NR; ++j) sts(xs_addr + (so ^ (swz((uint32_t)j << Q.reg_l) * 16u)), v[q][j]);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < NR; ++j) v[q][j] = lds(xs_addr + (sn ^ (swz((uint32_t)j << P.reg_l) * 16u)));
+      }
+      lb = nlb;
+    };
+
+    // ---------------------------------------------------------------- pass 1
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      if (p > 0) exchange(shape_phase(SH, p - 1), shape_phase(SH, p), std::integral_constant<int, NVA>{});
+      // FULL: compile-time gate mask (no branches around the register tile)
+      const uint32_t apply = FULL ? shape_apply(SH, p) : a.ph[p].apply;
+      if constexpr (NV == 2 && MODE != SM_BRIDGE) {
+        // sum_j <bra|X_j|ket> for this phase's qubits, before any of its gates
+        // (X_j commutes with every Rx): one scale factor xs_w[p] covers them
+        if (flags & SF_XSUM) acc2 = fma(a.xs_w[p], xsum_bits<NR, R>(v, apply), acc2);
+      }
+      gate_bits<FORM, NVA, NV, NR, R>(v, apply, a.ga, a.gb);
+    }
+
+    // ---------------------------------------------------------------- mid ops + pass 2
+    if constexpr (MODE != SM_PLAIN) {
+      constexpr int RM = shape_phase(SH, NP - 1).reg_l;
+      with_table([&](auto tv) {
+        const uint64_t g1 = base + gofs<IS_A>(lb, glo);
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+          const uint32_t l = lb | ((uint32_t)j << RM);
+          const uint64_t g = g1 + gofs<IS_A>((uint32_t)j << RM, glo);
+          if constexpr (MODE == SM_BRIDGE) {
+            const double t = tv.val(l, g);
+            if (flags & SF_MID_EXPECT) {
+              const double d = fma(v[0][j].x, v[0][j].x, v[0][j].y * v[0][j].y);
+              if (j & 1) acc0b = fma(t, d, acc0b);
+              else acc0 = fma(t, d, acc0);
+            }
+            v[1][j] = make_double2(t * v[0][j].x, t * v[0][j].y);
+          } else {
+            if constexpr (NV == 2) {
+              if (flags & SF_MID_DINNER) {
+                const double t = tv.val(l, g);
+                const double d = v[1][j].x * v[0][j].y - v[1][j].y * v[0][j].x;
+                if (j & 1) acc1b = fma(t, d, acc1b);
+                else acc1 = fma(t, d, acc1);
+              }
+            }
+            if (flags & SF_MID_PHASE) {
+              const double2 f = tv.phase(l, g);
+#pragma unroll
+              for (int q = 0; q < NV; ++q) v[q][j] = cmul_fast(v[q][j], f);
+            }
+          }
+        }
+      });
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp) {
+        const int p = NP - 1 - pp;
+        if (pp > 0) exchange(shape_phase(SH, p + 1), shape_phase(SH, p), std::integral_constant<int, NV>{});
+        const uint32_t apply = FULL ? shape_apply_rev(SH, p) : a.apply2[p];
+        if constexpr (NV == 2) {
+          if (flags & SF_XSUM2) acc3 = fma(a.xs_w2[p], xsum_bits<NR, R>(v, apply), acc3);
+        }
+        gate_bits<FORM2, NV, NV, NR, R>(v, apply, a.ga2, a.gb2);
       }
     }
 
     // ---------------------------------------------------------------- post
+    // the map the tile ends in: the last phase (plain) or the first (merged)
+    constexpr int RL = shape_phase(SH, MODE == SM_PLAIN ? NP - 1 : 0).reg_l;
     if constexpr (!EXACT) {  // factored gates: one real scale per sweep (1.0 if no gates)
       const double sc = a.post_scale;
 #pragma unroll
@@ -421,7 +478,25 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
 #pragma unroll
         for (int j = 0; j < NR; ++j) v[q][j] = make_double2(v[q][j].x * sc, v[q][j].y * sc);
     }
-    if (flags & (SF_POST_EXPECT | SF_POST_DINNER)) with_table([&](auto tv) { post_ops(tv, lb); });
+    if constexpr (MODE == SM_PLAIN) {
+      // post ops: <psi|C|psi> (NV=1) or <bra|C|ket> (NV=2) after the gates, in the last map
+      if (flags & (SF_POST_EXPECT | SF_POST_DINNER)) with_table([&](auto tv) {
+        const uint64_t g1 = base + gofs<IS_A>(lb, glo);
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+          const double t = tv.val(lb | ((uint32_t)j << RL), g1 + gofs<IS_A>((uint32_t)j << RL, glo));
+          double d;
+          if constexpr (NV == 1) d = fma(v[0][j].x, v[0][j].x, v[0][j].y * v[0][j].y);
+          else d = v[1][j].x * v[0][j].y - v[1][j].y * v[0][j].x;  // slot 0: PRE_DINNER may use slot 1
+          if (j & 1) acc0b = fma(t, d, acc0b);
+          else acc0 = fma(t, d, acc0);
+        }
+      });
+    }
+    // Order this tile's generic-proxy smem writes (exchanges) before the TMA that will
+    // refill the slot.  Fenced here, ahead of the global stores: the fence's MEMBAR
+    // then does not wait for this tile's 64-128 KB of stores to drain.
+    fence_proxy_async();
     if (!(flags & SF_NO_STORE)) {
       const uint64_t g1 = base + gofs<IS_A>(lb, glo);
 #pragma unroll
@@ -431,8 +506,7 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
         for (int j = 0; j < NR; ++j) st_stream(dst + gofs<IS_A>((uint32_t)j << RL, glo), v[q][j]);
       }
     }
-    fence_proxy_async();  // our generic-proxy smem writes before TMA refills the slot
-    __syncthreads();      // this tile's slots may be refilled from the next iteration on
+    __syncthreads();  // this tile's slots may be refilled from the next iteration on
   }
 
   // ------------------------------------------------------------ partial sums
@@ -441,32 +515,36 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
     acc0 = warp_sum(acc0 + acc0b);
     acc1 = warp_sum(acc1 + acc1b);
     acc2 = warp_sum(acc2);
+    acc3 = warp_sum(acc3);
     constexpr int NW = 1 << W;
     if (lane == 0) {
       red[warp] = acc0;
       red[NW + warp] = acc1;
       red[2 * NW + warp] = acc2;
+      red[3 * NW + warp] = acc3;
     }
     __syncthreads();
     if (threadIdx.x < kSlots) {
       double s = 0.0;
 #pragma unroll
       for (int w = 0; w < NW; ++w) s += red[threadIdx.x * NW + w];
-      a.partials[threadIdx.x * gridDim.x + blockIdx.x] = s;
+      // slots 0 / 1 of a merged sweep are taken before the final scale
+      const double wt = threadIdx.x == 0 ? a.w0 : threadIdx.x == 1 ? a.w1 : 1.0;
+      a.partials[threadIdx.x * gridDim.x + blockIdx.x] = s * wt;
     }
   }
 }
 
-template <int SH, int NV, int FORM, bool KSIN, bool FULL>
+template <int SH, int NV, int FORM, bool KSIN, bool FULL, int MODE = SM_PLAIN, int FORM2 = FORM>
 struct SweepKernel {
   static constexpr int threads = 32 << shape_w(SH);
   static int grid(qsb_ctx* ctx, uint64_t ntiles, unsigned* g) {
     static int occ = -1;  // per process; one device type
     if (occ < 0) {
-      QSB_CUDA(cudaFuncSetAttribute(k_sweep<SH, NV, FORM, KSIN, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      QSB_CUDA(cudaFuncSetAttribute(k_sweep<SH, NV, FORM, KSIN, FULL, MODE, FORM2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)kSmemBytes));
       int o = 0;
-      QSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sweep<SH, NV, FORM, KSIN, FULL>, threads, kSmemBytes));
+      QSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sweep<SH, NV, FORM, KSIN, FULL, MODE, FORM2>, threads, kSmemBytes));
       occ = o < 1 ? 1 : o;
     }
     const uint64_t want = (uint64_t)ctx->num_sms * occ;
@@ -476,7 +554,7 @@ struct SweepKernel {
   static int launch(qsb_ctx* ctx, SweepArgs& a, unsigned* gout) {
     unsigned g;
     QSB_TRY(grid(ctx, a.ntiles, &g));
-    k_sweep<SH, NV, FORM, KSIN, FULL><<<g, threads, kSmemBytes, ctx->stream>>>(a);
+    k_sweep<SH, NV, FORM, KSIN, FULL, MODE, FORM2><<<g, threads, kSmemBytes, ctx->stream>>>(a);
     QSB_CHECK_LAUNCH(ctx, "sweep");
     if (gout) *gout = g;
     return QSB_OK;
@@ -500,6 +578,31 @@ int launch_fast(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
   }
   if (a.full) return c ? L(SweepKernel<SB, NV, GF_FACT_C, false, true>{}) : L(SweepKernel<SB, NV, GF_FACT_S, false, true>{});
   return c ? L(SweepKernel<SB, NV, GF_FACT_C, false, false>{}) : L(SweepKernel<SB, NV, GF_FACT_S, false, false>{});
+}
+
+// merged / bridge instantiations (fast mode, R=4 family: A2 / B2).  Table ops between
+// the passes dispatch on the table kind at run time (KSIN = false).
+template <int NV, int MODE, int F1>
+int launch_merged_f1(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
+  auto L = [&](auto k) { return decltype(k)::launch(ctx, a, g); };
+  const bool c2 = a.form2 == GF_FACT_C;
+  if constexpr (MODE == SM_BRIDGE) {  // Rx(-2b) then Rx(+2b): the same form
+    if (a.shape == SH_A2) return a.full ? L(SweepKernel<SH_A2, NV, F1, false, true, MODE, F1>{})
+                                        : L(SweepKernel<SH_A2, NV, F1, false, false, MODE, F1>{});
+    return a.full ? L(SweepKernel<SH_B2, NV, F1, false, true, MODE, F1>{})
+                  : L(SweepKernel<SH_B2, NV, F1, false, false, MODE, F1>{});
+  } else {
+    if (a.shape == SH_A2) {
+      if (a.full) return c2 ? L(SweepKernel<SH_A2, NV, F1, false, true, MODE, GF_FACT_C>{})
+                            : L(SweepKernel<SH_A2, NV, F1, false, true, MODE, GF_FACT_S>{});
+      return c2 ? L(SweepKernel<SH_A2, NV, F1, false, false, MODE, GF_FACT_C>{})
+                : L(SweepKernel<SH_A2, NV, F1, false, false, MODE, GF_FACT_S>{});
+    }
+    if (a.full) return c2 ? L(SweepKernel<SH_B2, NV, F1, false, true, MODE, GF_FACT_C>{})
+                          : L(SweepKernel<SH_B2, NV, F1, false, true, MODE, GF_FACT_S>{});
+    return c2 ? L(SweepKernel<SH_B2, NV, F1, false, false, MODE, GF_FACT_C>{})
+              : L(SweepKernel<SH_B2, NV, F1, false, false, MODE, GF_FACT_S>{});
+  }
 }
 
 // exact-mode instantiations (ascending qubit order, FMA-free): shapes A2X / B2

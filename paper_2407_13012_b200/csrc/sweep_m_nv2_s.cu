@@ -1,0 +1,8 @@
+// Merged-sweep instantiations (two gate passes per HBM pass): NV=2, first-pass form S.
+#include "sweep_impl.cuh"
+
+namespace qsb {
+int launch_sweep_m_nv2_s(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
+  return sweepk::launch_merged_f1<2, SM_MERGED, GF_FACT_S>(ctx, a, g);
+}
+}  // namespace qsb

@@ -1,0 +1,91 @@
+"""The merged window chain (fused.cu run_chain): consecutive layers meet on the same
+window and share one HBM pass (merged / bridge sweeps).  Parity: the chain must
+agree with the one-visit-per-sweep schedule (QSB_NO_MERGE=1) to ~1e-12 and with the
+CPU oracle (the reference's op sequence) within the north-star 1e-10, across
+register sizes whose windows are partial (odd n, n - 12 not a multiple of 9), both
+gate forms (|cos| >= |sin| and below) and the float-weight (device sincos) table."""
+
+import numpy as np
+import pytest
+
+import paper_2407_13012_b200 as qs
+
+from conftest import random_instance, random_params, rel_err
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def flat(g):
+    out = np.empty(2 * g.p)
+    out[0::2] = g.d_gammas
+    out[1::2] = g.d_betas
+    return out
+
+
+def run(poly, params, monkeypatch, merge):
+    monkeypatch.setenv("QSB_NO_MERGE", "0" if merge else "1")
+    h = qs.create_handle(poly, backend_name="b200")
+    v, g = qs.value_and_grad(h, params)
+    e = qs.expectation(h, params)
+    psi = np.asarray(qs.statevector(h, params))
+    h.close()
+    return v, flat(g), e, psi
+
+
+def params_wide(seed, p):
+    """angles over (-pi, pi): both factored gate forms occur"""
+    rs = np.random.default_rng(seed)
+    return qs.QaoaParams(list(rs.uniform(-3.0, 3.0, p)), list(rs.uniform(-1.5, 1.5, p)))
+
+
+@pytest.mark.parametrize("n,p", [(12, 2), (13, 1), (13, 3), (16, 2), (21, 2), (22, 3), (24, 1)])
+def test_chain_vs_oracle(n, p, monkeypatch):
+    poly = random_instance(1000 + n * 7 + p, n)
+    params = params_wide(n * 31 + p, p)
+    v, g, e, psi = run(poly, params, monkeypatch, merge=True)
+    table = oracle.precompute_table(poly.weights, poly.masks, n)
+    want_psi = oracle.simulate(table, n, params.gammas, params.betas)
+    want_e = oracle.expectation(table, want_psi)
+    dg, db = oracle.gradient(table, want_psi.copy(), params.gammas, params.betas)
+    want = np.empty(2 * p)
+    want[0::2], want[1::2] = dg, db
+    assert abs(v - want_e) <= 1e-10 * max(1.0, abs(want_e))
+    assert abs(e - want_e) <= 1e-10 * max(1.0, abs(want_e))
+    assert rel_err(g, want) <= 1e-10
+    assert rel_err(psi, want_psi) <= 1e-10
+
+
+@pytest.mark.parametrize("n,p", [(25, 2), (27, 3), (28, 2), (30, 1)])
+def test_chain_vs_unmerged(n, p, monkeypatch):
+    """3-window registers (partial last window at n = 25, 27, 28) against the
+    unmerged schedule on the same GPU"""
+    poly = random_instance(77 + n, n)
+    params = params_wide(5 * n + p, p)
+    got = run(poly, params, monkeypatch, merge=True)
+    ref = run(poly, params, monkeypatch, merge=False)
+    assert abs(got[0] - ref[0]) <= 1e-12 * max(1.0, abs(ref[0]))
+    assert rel_err(got[1], ref[1]) <= 1e-12
+    assert abs(got[2] - ref[2]) <= 1e-12 * max(1.0, abs(ref[2]))
+    assert rel_err(got[3], ref[3]) <= 1e-12
+    assert abs(np.vdot(got[3], got[3]).real - 1.0) <= 1e-10
+
+
+def test_chain_float_table(monkeypatch):
+    """dense QUBO with float weights: f64 table + device sincos inside merged sweeps"""
+    n, p = 18, 3
+    rs = np.random.default_rng(3)
+    terms = [((rs.random() - 0.5) * 8.0, 1 << i) for i in range(n)]
+    terms += [((rs.random() - 0.5) * 8.0, (1 << i) | (1 << j)) for i in range(n) for j in range(i + 1, n) if rs.random() < 0.5]
+    poly = qs.Polynomial(n, terms)
+    params = params_wide(9, p)
+    v, g, e, psi = run(poly, params, monkeypatch, merge=True)
+    table = oracle.precompute_table(poly.weights, poly.masks, n)
+    want_psi = oracle.simulate(table, n, params.gammas, params.betas)
+    want_e = oracle.expectation(table, want_psi)
+    dg, db = oracle.gradient(table, want_psi.copy(), params.gammas, params.betas)
+    want = np.empty(2 * p)
+    want[0::2], want[1::2] = dg, db
+    assert abs(v - want_e) <= 1e-10 * max(1.0, abs(want_e))
+    assert rel_err(g, want) <= 1e-10
+    assert rel_err(psi, want_psi) <= 1e-10
