@@ -50,17 +50,17 @@ std::vector<SweepShape> plan_range(int n, int lo, int hi) {
 
 std::vector<SweepShape> plan_sweeps(int n) { return plan_range(n, 0, n - 1); }
 
-// register-bit family of the fast sweeps (QSB_SWEEP_R1 / QSB_SWEEP_R2 override)
-int sweep_family(int nv) {
-  static int fam[3] = {0, 0, 0};
-  if (!fam[nv]) {
-    const char* e = getenv(nv == 1 ? "QSB_SWEEP_R1" : "QSB_SWEEP_R2");
-    int r = e ? atoi(e) : 0;
-    if (nv == 2 && r == 5) r = 0;  // two vectors of 32 amplitudes do not fit in registers
-    if (r < 3 || r > 5) r = 4;  // measured best for both kinds on B200 (profiles/)
-    fam[nv] = r;
-  }
-  return fam[nv];
+// register-bit family of the fast sweeps: 4 by default; overrides QSB_SWEEP_R1 /
+// QSB_SWEEP_R2 (plain sweeps, 3..5 / 3..4) and QSB_SWEEP_R1M (merged single-vector
+// sweeps, 4 or 5; merged bra/ket sweeps are R=4 only)
+int sweep_family(int nv, bool merged) {
+  if (merged && nv == 2) return 4;
+  const char* e = getenv(merged ? "QSB_SWEEP_R1M" : (nv == 1 ? "QSB_SWEEP_R1" : "QSB_SWEEP_R2"));
+  int r = e ? atoi(e) : 4;
+  if (merged) return r == 5 ? 5 : 4;
+  if (nv == 2 && r == 5) r = 4;  // two vectors of 32 amplitudes do not fit in registers
+  if (r < 3 || r > 5) r = 4;
+  return r;
 }
 
 // Fill the tile/phase part of SweepArgs for one sweep. Returns the number of gates.
@@ -68,7 +68,7 @@ int build_shape(const SweepShape& sh, int n, int nv, bool exact, SweepArgs& a, i
                 const int* pass2 = nullptr, int gates_before_phase2[kMaxPhases] = nullptr, int* gates2 = nullptr) {
   int gl[kSweepT];
   for (int i = 0; i < kSweepT; ++i) gl[i] = sh.is_a ? i : (i < 3 ? i : sh.glo + i - 3);
-  const int shape = pick_shape(exact, sh.is_a, sweep_family(nv));
+  const int shape = pick_shape(exact, sh.is_a, sweep_family(nv, pass2 != nullptr));
   const int np = shape_np(shape);
   PhaseSpec ps[kMaxPhases];
   for (int p = 0; p < np; ++p) ps[p] = shape_phase(shape, p);
@@ -312,7 +312,7 @@ struct Runner {
       b += (mode == SM_BRIDGE || (flags & SF_BRA_FROM_KET)) ? 16.0 * N : 32.0 * N;
       if (!(flags & SF_NO_STORE)) b += 32.0 * N;
     }
-    if (flags & kTableOps) b += tb * N;
+    if ((flags & kTableOps) || mode == SM_BRIDGE) b += tb * N;
     return b;
   }
 
@@ -342,7 +342,9 @@ struct Runner {
     a.v0 = v0;
     a.v1 = v1;
     set_table(a, t);
-    a.cmode = (t && t->kind != 0 && (flags & kTableOps)) ? ((!sh.is_a && t->kind == 1) ? 2 : 1) : 0;
+    // (a bridge always reads the table: bra = C * ket between its passes)
+    const bool table_ops = (flags & kTableOps) || mode == SM_BRIDGE;
+    a.cmode = (t && t->kind != 0 && table_ops) ? ((!sh.is_a && t->kind == 1) ? 2 : 1) : 0;
     if (!sh.is_a) {  // TMA boxes for the strided B tiles
       QSB_TRY(encode_b_tile_map(&a.tm0, v0, n, sh.glo));
       if (nv == 2) QSB_TRY(encode_b_tile_map(&a.tm1, v1, n, sh.glo));
@@ -356,7 +358,12 @@ struct Runner {
     a.gb = g1.gb;
     a.plus_amp = plus_amp > 0.0 ? plus_amp : 1.0 / sqrt((double)(1ull << n));
     const double s1 = g1.sigma * g1.sigma;
-    for (int p = 0; p < kMaxPhases; ++p) a.xs_w[p] = ipow(s1, gbp[p]);
+    // xsum weights: the pending gate scale^2 where the kernel takes the xsum (fast: after
+    // the phase's gates; exact: sigma = 1)
+    auto after = [](const int* gb, const uint8_t* ap, int p) { return gb[p] + __builtin_popcount(ap[p]); };
+    uint8_t ap1[kMaxPhases];
+    for (int p = 0; p < kMaxPhases; ++p) ap1[p] = a.ph[p].apply;
+    for (int p = 0; p < a.nphase; ++p) a.xs_w[p] = ipow(s1, exact ? gbp[p] : after(gbp, ap1, p));
     a.w0 = a.w1 = 1.0;
     if (mode != SM_PLAIN) {
       // pass-1 scale is still pending at the mid ops and throughout pass 2
@@ -365,7 +372,7 @@ struct Runner {
       a.form2 = g2.form;
       a.ga2 = g2.ga;
       a.gb2 = g2.gb;
-      for (int p = 0; p < kMaxPhases; ++p) a.xs_w2[p] = m * ipow(g2.sigma * g2.sigma, gbp2[p]);
+      for (int p = 0; p < a.nphase; ++p) a.xs_w2[p] = m * ipow(g2.sigma * g2.sigma, after(gbp2, a.apply2, p));
       a.post_scale = ipow(g1.sigma, gates) * ipow(g2.sigma, gates2);
       if (gates + gates2 > 0) flags |= SF_POST_SCALE;
     } else {

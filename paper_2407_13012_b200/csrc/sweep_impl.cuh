@@ -269,15 +269,21 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
   double acc0 = 0.0, acc0b = 0.0, acc1 = 0.0, acc1b = 0.0, acc2 = 0.0, acc3 = 0.0;
   double2 v[NV][NR];
 
+  // NV=1: tile k lands in slot k % 3, two tiles in flight.  NV=2: bra / ket of tile k
+  // in slots 2k % 3 / (2k+1) % 3, both used for the exchanges; after the tile's last
+  // exchange they are refilled with the ket of tile k+1 and the bra of tile k+2
+  // (the bra of tile k+1 is already in flight in the third slot).
   issue(0);
   issue(1);
+  if constexpr (NV == 2) issue(2);
   for (uint64_t k = 0; k < my_tiles; ++k) {
     const uint64_t base = tile_base(a, blockIdx.x + k * gridDim.x);
     const uint8_t* cs = cring + (uint32_t)(k % kRing) * kCBytes;
     const uint32_t tb8 = (uint32_t)((blockIdx.x + k * gridDim.x) & 1u) << 3;  // cmode 2: tile's half of each row
     constexpr PhaseSpec P0 = shape_phase(SH, 0);
     uint32_t lb = lbase<W>(P0, lane, warp);
-    uint32_t xs_addr;  // byte address of the exchange slot for this tile
+    uint32_t xs_addr;      // byte address of the exchange slot for this tile (ket for NV=2)
+    uint32_t xb_addr = 0;  // NV=2: the bra's slot
 
     // Loads are unconditional (a skipped TMA leaves stale data that is overwritten
     // below): no branch around the register tile, hence no phi-moves of it.
@@ -293,19 +299,15 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
         v[0][j] = make_double2(plus ? a.plus_amp : x.x, plus ? 0.0 : x.y);
       }
     } else {
-      issue(2 * k + 2);  // bra of the next tile into the slot freed at the end of tile k-1
-      wait_seq(2 * k);
-      wait_seq(2 * k + 1);
-      const uint32_t b_addr = ring_s + (uint32_t)((2 * k) % kRing) * kSlotBytes;
+      xb_addr = ring_s + (uint32_t)((2 * k) % kRing) * kSlotBytes;
       xs_addr = ring_s + (uint32_t)((2 * k + 1) % kRing) * kSlotBytes;
-      const uint32_t pb = b_addr + lb * 16u;
+      wait_seq(2 * k);
       if constexpr (MODE != SM_BRIDGE) {
+        const uint32_t pb = xb_addr + lb * 16u;
 #pragma unroll
         for (int j = 0; j < NR; ++j) v[1][j] = lds(pb + (((uint32_t)j << P0.reg_l) * 16u));
       }
-      fence_proxy_async();
-      __syncthreads();
-      issue(2 * k + 3);  // ket of the next tile into the bra slot just read
+      wait_seq(2 * k + 1);
       const uint32_t p0 = xs_addr + lb * 16u;
 #pragma unroll
       for (int j = 0; j < NR; ++j) v[0][j] = lds(p0 + (((uint32_t)j << P0.reg_l) * 16u));
@@ -392,34 +394,65 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
     }  // merged sweeps start and end mid-layer: no pre / post ops
 
     // exchange the register tile from phase map Q to phase map P through this tile's
-    // slot (swizzled), one vector at a time
+    // slot(s) (swizzled): NV=1 through its one slot, NV=2 the ket and the bra through
+    // their own slots at once.  When Q and P put the same local bits on the warp
+    // index, every warp reads back only what it wrote (the swizzle keeps bits >= 3
+    // fixed, and warp bits are >= 5): a warp barrier suffices.
     auto exchange = [&](const PhaseSpec Q, const PhaseSpec P, auto nvx) {
+      bool local = true;
+#pragma unroll
+      for (int b = 0; b < W; ++b) local = local && Q.warps[b] == P.warps[b];
       const uint32_t nlb = lbase<W>(P, lane, warp);
       const uint32_t so = swz(lb) * 16u, sn = swz(nlb) * 16u;
+      if (local) __syncwarp(); else __syncthreads();
 #pragma unroll
       for (int q = 0; q < decltype(nvx)::value; ++q) {
-        __syncthreads();
+        const uint32_t xa = q == 0 ? xs_addr : xb_addr;
 #pragma unroll
-        for (int j = 0; j < NR; ++j) sts(xs_addr + (so ^ (swz((uint32_t)j << Q.reg_l) * 16u)), v[q][j]);
-        __syncthreads();
+        for (int j = 0; j < NR; ++j) sts(xa + (so ^ (swz((uint32_t)j << Q.reg_l) * 16u)), v[q][j]);
+      }
+      if (local) __syncwarp(); else __syncthreads();
 #pragma unroll
-        for (int j = 0; j < NR; ++j) v[q][j] = lds(xs_addr + (sn ^ (swz((uint32_t)j << P.reg_l) * 16u)));
+      for (int q = 0; q < decltype(nvx)::value; ++q) {
+        const uint32_t xa = q == 0 ? xs_addr : xb_addr;
+#pragma unroll
+        for (int j = 0; j < NR; ++j) v[q][j] = lds(xa + (sn ^ (swz((uint32_t)j << P.reg_l) * 16u)));
       }
       lb = nlb;
+    };
+    // NV=2: after the tile's last exchange both slots are free -> refill them.  The
+    // fence orders this tile's generic-proxy smem writes before the TMA writes.
+    auto release = [&]() {
+      if constexpr (NV == 2) {
+        fence_proxy_async();
+        __syncthreads();
+        issue(2 * k + 3);
+        issue(2 * k + 4);
+      }
+    };
+    // sum_j <bra|X_j|ket> over this phase's gated qubits.  X_j commutes with every Rx,
+    // so any point of the layer where both vectors carry the same gates gives the same
+    // value: fast mode takes it after the phase's gates (xs_w = the pending scale^2
+    // then), exact mode before them (the reference's order).
+    auto xsum = [&](double& acc, double w, uint32_t apply) {
+      if constexpr (NV == 2) acc = fma(w, xsum_bits<NR, R>(v, apply), acc);
     };
 
     // ---------------------------------------------------------------- pass 1
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       if (p > 0) exchange(shape_phase(SH, p - 1), shape_phase(SH, p), std::integral_constant<int, NVA>{});
+      if (MODE == SM_PLAIN && p == NP - 1) release();
       // FULL: compile-time gate mask (no branches around the register tile)
       const uint32_t apply = FULL ? shape_apply(SH, p) : a.ph[p].apply;
-      if constexpr (NV == 2 && MODE != SM_BRIDGE) {
-        // sum_j <bra|X_j|ket> for this phase's qubits, before any of its gates
-        // (X_j commutes with every Rx): one scale factor xs_w[p] covers them
-        if (flags & SF_XSUM) acc2 = fma(a.xs_w[p], xsum_bits<NR, R>(v, apply), acc2);
+      constexpr bool XS1 = NV == 2 && MODE != SM_BRIDGE;
+      if constexpr (XS1 && EXACT) {
+        if (flags & SF_XSUM) xsum(acc2, a.xs_w[p], apply);
       }
       gate_bits<FORM, NVA, NV, NR, R>(v, apply, a.ga, a.gb);
+      if constexpr (XS1 && !EXACT) {
+        if (flags & SF_XSUM) xsum(acc2, a.xs_w[p], apply);
+      }
     }
 
     // ---------------------------------------------------------------- mid ops + pass 2
@@ -460,11 +493,10 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
       for (int pp = 0; pp < NP; ++pp) {
         const int p = NP - 1 - pp;
         if (pp > 0) exchange(shape_phase(SH, p + 1), shape_phase(SH, p), std::integral_constant<int, NV>{});
+        if (pp == NP - 1) release();
         const uint32_t apply = FULL ? shape_apply_rev(SH, p) : a.apply2[p];
-        if constexpr (NV == 2) {
-          if (flags & SF_XSUM2) acc3 = fma(a.xs_w2[p], xsum_bits<NR, R>(v, apply), acc3);
-        }
         gate_bits<FORM2, NV, NV, NR, R>(v, apply, a.ga2, a.gb2);
+        if (flags & SF_XSUM2) xsum(acc3, a.xs_w2[p], apply);
       }
     }
 
@@ -493,10 +525,10 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
         }
       });
     }
-    // Order this tile's generic-proxy smem writes (exchanges) before the TMA that will
-    // refill the slot.  Fenced here, ahead of the global stores: the fence's MEMBAR
-    // then does not wait for this tile's 64-128 KB of stores to drain.
-    fence_proxy_async();
+    // NV=1: order this tile's generic-proxy smem writes (exchanges) before the TMA that
+    // will refill the slot.  Fenced here, ahead of the global stores: the fence's
+    // MEMBAR then does not wait for this tile's 64 KB of stores to drain.
+    if constexpr (NV == 1) fence_proxy_async();
     if (!(flags & SF_NO_STORE)) {
       const uint64_t g1 = base + gofs<IS_A>(lb, glo);
 #pragma unroll
@@ -506,12 +538,13 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
         for (int j = 0; j < NR; ++j) st_stream(dst + gofs<IS_A>((uint32_t)j << RL, glo), v[q][j]);
       }
     }
-    __syncthreads();  // this tile's slots may be refilled from the next iteration on
+    if constexpr (NV == 1) __syncthreads();  // the slot may be refilled from the next iteration on
   }
 
   // ------------------------------------------------------------ partial sums
   if (a.partials) {
     double* red = (double*)smem_raw;
+    __syncthreads();
     acc0 = warp_sum(acc0 + acc0b);
     acc1 = warp_sum(acc1 + acc1b);
     acc2 = warp_sum(acc2);
@@ -580,28 +613,28 @@ int launch_fast(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
   return c ? L(SweepKernel<SB, NV, GF_FACT_C, false, false>{}) : L(SweepKernel<SB, NV, GF_FACT_S, false, false>{});
 }
 
-// merged / bridge instantiations (fast mode, R=4 family: A2 / B2).  Table ops between
+// merged / bridge instantiations (fast mode; shapes SA / SB of one register family).  Table ops between
 // the passes dispatch on the table kind at run time (KSIN = false).
-template <int NV, int MODE, int F1>
+template <int NV, int MODE, int F1, int SA = SH_A2, int SB = SH_B2>
 int launch_merged_f1(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
   auto L = [&](auto k) { return decltype(k)::launch(ctx, a, g); };
   const bool c2 = a.form2 == GF_FACT_C;
   if constexpr (MODE == SM_BRIDGE) {  // Rx(-2b) then Rx(+2b): the same form
-    if (a.shape == SH_A2) return a.full ? L(SweepKernel<SH_A2, NV, F1, false, true, MODE, F1>{})
-                                        : L(SweepKernel<SH_A2, NV, F1, false, false, MODE, F1>{});
-    return a.full ? L(SweepKernel<SH_B2, NV, F1, false, true, MODE, F1>{})
-                  : L(SweepKernel<SH_B2, NV, F1, false, false, MODE, F1>{});
+    if (a.shape == SA) return a.full ? L(SweepKernel<SA, NV, F1, false, true, MODE, F1>{})
+                                        : L(SweepKernel<SA, NV, F1, false, false, MODE, F1>{});
+    return a.full ? L(SweepKernel<SB, NV, F1, false, true, MODE, F1>{})
+                  : L(SweepKernel<SB, NV, F1, false, false, MODE, F1>{});
   } else {
-    if (a.shape == SH_A2) {
-      if (a.full) return c2 ? L(SweepKernel<SH_A2, NV, F1, false, true, MODE, GF_FACT_C>{})
-                            : L(SweepKernel<SH_A2, NV, F1, false, true, MODE, GF_FACT_S>{});
-      return c2 ? L(SweepKernel<SH_A2, NV, F1, false, false, MODE, GF_FACT_C>{})
-                : L(SweepKernel<SH_A2, NV, F1, false, false, MODE, GF_FACT_S>{});
+    if (a.shape == SA) {
+      if (a.full) return c2 ? L(SweepKernel<SA, NV, F1, false, true, MODE, GF_FACT_C>{})
+                            : L(SweepKernel<SA, NV, F1, false, true, MODE, GF_FACT_S>{});
+      return c2 ? L(SweepKernel<SA, NV, F1, false, false, MODE, GF_FACT_C>{})
+                : L(SweepKernel<SA, NV, F1, false, false, MODE, GF_FACT_S>{});
     }
-    if (a.full) return c2 ? L(SweepKernel<SH_B2, NV, F1, false, true, MODE, GF_FACT_C>{})
-                          : L(SweepKernel<SH_B2, NV, F1, false, true, MODE, GF_FACT_S>{});
-    return c2 ? L(SweepKernel<SH_B2, NV, F1, false, false, MODE, GF_FACT_C>{})
-              : L(SweepKernel<SH_B2, NV, F1, false, false, MODE, GF_FACT_S>{});
+    if (a.full) return c2 ? L(SweepKernel<SB, NV, F1, false, true, MODE, GF_FACT_C>{})
+                          : L(SweepKernel<SB, NV, F1, false, true, MODE, GF_FACT_S>{});
+    return c2 ? L(SweepKernel<SB, NV, F1, false, false, MODE, GF_FACT_C>{})
+              : L(SweepKernel<SB, NV, F1, false, false, MODE, GF_FACT_S>{});
   }
 }
 

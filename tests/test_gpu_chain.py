@@ -89,3 +89,29 @@ def test_chain_float_table(monkeypatch):
     assert abs(v - want_e) <= 1e-10 * max(1.0, abs(want_e))
     assert rel_err(g, want) <= 1e-10
     assert rel_err(psi, want_psi) <= 1e-10
+
+
+@pytest.mark.parametrize("n,p", [(21, 2), (27, 2), (30, 2)])
+def test_chain_register_families(n, p, monkeypatch):
+    """merged single-vector sweeps with 32 amplitudes per thread (R=5: B windows need
+    one exchange per pass) against the default R=4 family"""
+    poly = random_instance(300 + n, n)
+    params = params_wide(11 * n + p, p)
+    ref = run(poly, params, monkeypatch, merge=True)
+    monkeypatch.setenv("QSB_SWEEP_R1M", "5")
+    got = run(poly, params, monkeypatch, merge=True)
+    assert abs(got[0] - ref[0]) <= 1e-12 * max(1.0, abs(ref[0]))
+    assert rel_err(got[1], ref[1]) <= 1e-12
+    assert rel_err(got[3], ref[3]) <= 1e-12
+
+
+@pytest.mark.parametrize("n,p", [(16, 3), (30, 1)])
+def test_gradient_without_value(n, p, monkeypatch):
+    """gradient() asks for no <C>: the bridge sweep must still read the table (bra = C*ket)"""
+    poly = random_instance(500 + n, n)
+    params = params_wide(3 * n + p, p)
+    h = qs.create_handle(poly, backend_name="b200")
+    v, g = qs.value_and_grad(h, params)
+    g2 = qs.gradient(h, params)
+    h.close()
+    assert rel_err(flat(g2), flat(g)) <= 1e-13
