@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--p", type=int, default=DEPTH)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--params", choices=["ramp", "random"], default="ramp")
+    ap.add_argument("--shots", type=int, default=1_000_000)
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent n=30 replicas instead of sharding")
     return ap.parse_args()
 
@@ -404,6 +405,17 @@ def run_b200(args, rank: int, world: int, dist) -> None:
     sim_ms = dev.timer_stop()
     layers_per_s = args.p * args.steps / (sim_ms / 1e3)
 
+    # C3's 10^6 shots: draw from the simulated state (probability tree + per-shot
+    # descent + cost gather on the device; indices/costs copied to the host)
+    qs.simulate(h, params)
+    dev.sync()
+    dev.timer_start()
+    t0 = time.perf_counter()
+    shots = qs.draw(h, args.shots, 1)
+    sample_wall_ms = (time.perf_counter() - t0) * 1e3
+    sample_ms = dev.timer_stop()
+    best = qs.best_of(shots)
+
     if dist is not None:
         import torch
 
@@ -440,6 +452,8 @@ def run_b200(args, rank: int, world: int, dist) -> None:
         "layers_per_s": world * layers_per_s,
         "simulate_ms": sim_ms / args.steps,
         "precompute_s": precompute_s,
+        "sampling": {"shots": args.shots, "device_ms": sample_ms, "wall_ms": sample_wall_ms,
+                     "best_cost": best[1], "how": "qs.draw(handle, shots, seed=1) after simulate (C3)"},
         "gpu_launches": launches,
         "roofline": {
             "bound": "hbm",

@@ -51,15 +51,16 @@ std::vector<SweepShape> plan_range(int n, int lo, int hi) {
 std::vector<SweepShape> plan_sweeps(int n) { return plan_range(n, 0, n - 1); }
 
 // register-bit family of the fast sweeps: 4 by default; overrides QSB_SWEEP_R1 /
-// QSB_SWEEP_R2 (plain sweeps, 3..5 / 3..4) and QSB_SWEEP_R1M (merged single-vector
-// sweeps, 4 or 5; merged bra/ket sweeps are R=4 only)
+// QSB_SWEEP_R2 (plain sweeps, 3..6 / 3..4) and QSB_SWEEP_R1M (merged single-vector
+// sweeps, 4..6; merged bra/ket sweeps are R=4 only).  6 = the R=5 shapes with two
+// independent warp groups per CTA.
 int sweep_family(int nv, bool merged) {
   if (merged && nv == 2) return 4;
   const char* e = getenv(merged ? "QSB_SWEEP_R1M" : (nv == 1 ? "QSB_SWEEP_R1" : "QSB_SWEEP_R2"));
   int r = e ? atoi(e) : 4;
-  if (merged) return r == 5 ? 5 : 4;
-  if (nv == 2 && r == 5) r = 4;  // two vectors of 32 amplitudes do not fit in registers
-  if (r < 3 || r > 5) r = 4;
+  if (merged) return (r == 5 || r == 6) ? r : 4;
+  if (nv == 2 && r >= 5) r = 4;  // two vectors of 32 amplitudes do not fit in registers
+  if (r < 3 || r > 6) r = 4;
   return r;
 }
 
@@ -68,7 +69,9 @@ int build_shape(const SweepShape& sh, int n, int nv, bool exact, SweepArgs& a, i
                 const int* pass2 = nullptr, int gates_before_phase2[kMaxPhases] = nullptr, int* gates2 = nullptr) {
   int gl[kSweepT];
   for (int i = 0; i < kSweepT; ++i) gl[i] = sh.is_a ? i : (i < 3 ? i : sh.glo + i - 3);
-  const int shape = pick_shape(exact, sh.is_a, sweep_family(nv, pass2 != nullptr));
+  const int fam = exact ? 4 : sweep_family(nv, pass2 != nullptr);
+  const int shape = pick_shape(exact, sh.is_a, fam);
+  a.groups = fam == 6 ? 2 : 1;
   const int np = shape_np(shape);
   PhaseSpec ps[kMaxPhases];
   for (int p = 0; p < np; ++p) ps[p] = shape_phase(shape, p);

@@ -79,6 +79,7 @@ struct SweepArgs {
   uint8_t apply2[kMaxPhases];
   int form2;
   int mode;
+  int groups;             // warp groups per CTA (1, or 2 for the R=5 single-vector family "6")
   double* partials;       // [kSlots][gridDim.x]
   uint64_t ntiles;
   uint32_t flags;
@@ -191,11 +192,11 @@ __host__ __device__ constexpr uint32_t shape_apply_rev(int sh, int p) {
   return m;
 }
 
-// family r in {5, 4, 3} for fast mode; exact mode always uses the R=4 shapes
-// (ascending qubit order: A2X, B2)
+// family r in {6, 5, 4, 3} for fast mode (6 = the R=5 shapes run by two warp groups);
+// exact mode always uses the R=4 shapes (ascending qubit order: A2X, B2)
 __host__ __device__ constexpr int pick_shape(bool exact, bool is_a, int r) {
   return exact ? (is_a ? SH_A2X : SH_B2)
-       : r == 5 ? (is_a ? SH_A1 : SH_B1) : r == 4 ? (is_a ? SH_A2 : SH_B2) : (is_a ? SH_A3 : SH_B3);
+       : r >= 5 ? (is_a ? SH_A1 : SH_B1) : r == 4 ? (is_a ? SH_A2 : SH_B2) : (is_a ? SH_A3 : SH_B3);
 }
 
 // launch one sweep (picks the instantiation from a.shape / a.form / a.kind);

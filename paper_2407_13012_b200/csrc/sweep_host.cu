@@ -16,6 +16,9 @@ int launch_sweep_m_nv1_r4_c(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_m_nv1_r4_s(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_m_nv1_r5_c(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_m_nv1_r5_s(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int launch_sweep_m_nv1_r5g_c(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int launch_sweep_m_nv1_r5g_s(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int launch_sweep_nv1_r5g(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_m_nv2_c(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_m_nv2_s(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_bridge(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
@@ -29,6 +32,7 @@ int launch_sweep(qsb_ctx* ctx, int nv, bool exact, SweepArgs& a, unsigned* gout)
     if (a.mode == SM_BRIDGE) return nv == 2 ? launch_sweep_bridge(ctx, a, gout) : invalid("internal: bridge needs nv=2");
     const bool c = a.form == GF_FACT_C;
     if (nv == 1) {
+      if (r == 5 && a.groups == 2) return c ? launch_sweep_m_nv1_r5g_c(ctx, a, gout) : launch_sweep_m_nv1_r5g_s(ctx, a, gout);
       if (r == 5) return c ? launch_sweep_m_nv1_r5_c(ctx, a, gout) : launch_sweep_m_nv1_r5_s(ctx, a, gout);
       return c ? launch_sweep_m_nv1_r4_c(ctx, a, gout) : launch_sweep_m_nv1_r4_s(ctx, a, gout);
     }
@@ -36,6 +40,7 @@ int launch_sweep(qsb_ctx* ctx, int nv, bool exact, SweepArgs& a, unsigned* gout)
   }
   if (exact || a.form == GF_EXACT) return nv == 1 ? launch_sweep_exact_nv1(ctx, a, gout) : launch_sweep_exact_nv2(ctx, a, gout);
   const int r = shape_r(a.shape);
+  if (nv == 1 && r == 5 && a.groups == 2) return launch_sweep_nv1_r5g(ctx, a, gout);
   if (nv == 1) return r == 5 ? launch_sweep_nv1_r5(ctx, a, gout) : r == 4 ? launch_sweep_nv1_r4(ctx, a, gout)
                                                                            : launch_sweep_nv1_r3(ctx, a, gout);
   if (r == 5) return invalid("internal: no R=5 bra/ket sweep");

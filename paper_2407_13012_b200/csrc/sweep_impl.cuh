@@ -185,9 +185,14 @@ __device__ __forceinline__ double xsum_bits(const double2 (&v)[2][NR], uint32_t 
 // SH: shape, NV: vectors (1 or 2), FORM: gate arithmetic, KSIN: f64 table +
 // device sincos (else compact index + LUT), FULL: every window position is a
 // target (gate masks fixed at compile time by the shape), MODE: SweepMode,
-// FORM2: gate arithmetic of the second pass (merged / bridge sweeps).
-template <int SH, int NV, int FORM, bool KSIN, bool FULL, int MODE, int FORM2>
-__global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_constant__ SweepArgs a) {
+// FORM2: gate arithmetic of the second pass (merged / bridge sweeps), GR: warp
+// groups per CTA.  With GR = 2 (single-vector sweeps) the CTA holds two independent
+// groups of 2^W warps, each working through every other tile with its own named
+// barrier, so one group's shared-memory exchanges overlap the other's FP64 gates.
+// FM: the flags this instantiation may see (a compile-time mask; code for the others
+// is dropped, which keeps the common sweeps lean in registers and instructions).
+template <int SH, int NV, int FORM, bool KSIN, bool FULL, int MODE, int FORM2, int GR, uint32_t FM>
+__global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __grid_constant__ SweepArgs a) {
   constexpr int R = shape_r(SH), W = shape_w(SH), NP = shape_np(SH);
   constexpr bool IS_A = shape_is_a(SH);
   constexpr bool EXACT = FORM == GF_EXACT;
@@ -197,6 +202,7 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
   static_assert(5 + W + R == kSweepT, "tile size");
   static_assert(MODE == SM_PLAIN || !EXACT, "merged sweeps are fast-mode only");
   static_assert(MODE != SM_BRIDGE || NV == 2, "a bridge sweep produces the bra");
+  static_assert(GR == 1 || (GR == 2 && NV == 1), "warp groups: single-vector sweeps only");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(smem_raw);
   const uint32_t cring_s = ring_s + kRing * kSlotBytes;
@@ -204,8 +210,9 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
   double2* slut = (double2*)(cring + kRing * kCBytes);
   const uint32_t bar_s = ring_s + kRing * kSlotBytes + kRing * kCBytes + 256 * 16;
 
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t flags = a.flags;
+  const int tid = threadIdx.x & (NT - 1), grp = GR == 1 ? 0 : (int)(threadIdx.x / NT);
+  const int lane = tid & 31, warp = tid >> 5;  // within the group
+  const uint32_t flags = a.flags & FM;
   const int glo = a.glo;
   // compact-index tiles ride the TMA of the tile's first vector (cmode, see sweep.cuh)
   const int cmode = KSIN ? 0 : a.cmode;
@@ -213,26 +220,33 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
 
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int s = 0; s < kRing; ++s) mbar_init(bar_s + 8 * s, 1);
+    for (int s = 0; s < GR * kRing; ++s) mbar_init(bar_s + 8 * s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (!KSIN && a.kind == 1 && (flags & (SF_PRE_PHASE | SF_MID_PHASE))) {  // u8 LUT in smem
-    for (int i = threadIdx.x; i < a.nlut; i += NT) slut[i] = a.lut[i];
+    for (int i = threadIdx.x; i < a.nlut; i += GR * NT) slut[i] = a.lut[i];
   }
   __syncthreads();
 
   const uint64_t my_tiles = a.ntiles > blockIdx.x ? (a.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   const uint64_t nseq = my_tiles * NV;
 
-  // producer (thread 0): sequence s -> slot s % 3.  NV=1: tile s; NV=2: even = bra
-  // (v1) of tile s/2, odd = ket (v0).
+  // Full barrier of sequence s: one per slot; with GR=2 one per (group, slot), so a
+  // barrier only ever has one outstanding phase (tile s and s+6 are consumed by the
+  // same group in order, and tile s+6 is issued only after tile s+3, hence s, is done).
+  auto seq_bar = [&](uint64_t s) {
+    const uint32_t b = (uint32_t)(s % kRing) + (GR == 2 ? 3u * (uint32_t)(s & 1) : 0u);
+    return bar_s + 8u * b;
+  };
+  // producer (thread 0 of a group): sequence s -> slot s % 3.  NV=1: tile s; NV=2:
+  // even = bra (v1) of tile s/2, odd = ket (v0).
   auto issue = [&](uint64_t s) {
-    if (threadIdx.x != 0 || s >= nseq) return;
+    if (tid != 0 || s >= nseq) return;
     const uint64_t k = s / NV;
     const int q = NV == 2 ? (int)((s & 1) ^ 1) : 0;
     const uint64_t tile = blockIdx.x + k * gridDim.x;
     const uint32_t slot = (uint32_t)(s % kRing);
-    const uint32_t bar = bar_s + 8 * slot;
+    const uint32_t bar = seq_bar(s);
     const bool vec = !((q == 0 && (flags & SF_PLUS)) ||
                        (q == 1 && (MODE == SM_BRIDGE || (flags & SF_BRA_FROM_KET))));
     const bool cid = cmode != 0 && (s % NV) == 0;
@@ -264,7 +278,12 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
       }
     }
   };
-  auto wait_seq = [&](uint64_t s) { mbar_wait(bar_s + 8 * (uint32_t)(s % kRing), (uint32_t)((s / kRing) & 1)); };
+  // group barrier
+  auto gsync = [&]() {
+    if constexpr (GR == 1) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(NT) : "memory");
+  };
+  auto wait_seq = [&](uint64_t s) { mbar_wait(seq_bar(s), (uint32_t)((s / (GR * kRing)) & 1)); };
 
   double acc0 = 0.0, acc0b = 0.0, acc1 = 0.0, acc1b = 0.0, acc2 = 0.0, acc3 = 0.0;
   double2 v[NV][NR];
@@ -273,10 +292,15 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
   // in slots 2k % 3 / (2k+1) % 3, both used for the exchanges; after the tile's last
   // exchange they are refilled with the ket of tile k+1 and the bra of tile k+2
   // (the bra of tile k+1 is already in flight in the third slot).
-  issue(0);
-  issue(1);
-  if constexpr (NV == 2) issue(2);
-  for (uint64_t k = 0; k < my_tiles; ++k) {
+  // GR=2: tile k in slot k % 3; the group finishing tile k refills its slot with tile
+  // k+3 (the other group's next-but-one), so every tile is in flight for about one
+  // group-tile time.
+  if (grp == 0) {
+    issue(0);
+    issue(1);
+    if constexpr (NV == 2 || GR == 2) issue(2);
+  }
+  for (uint64_t k = grp; k < my_tiles; k += GR) {
     const uint64_t base = tile_base(a, blockIdx.x + k * gridDim.x);
     const uint8_t* cs = cring + (uint32_t)(k % kRing) * kCBytes;
     const uint32_t tb8 = (uint32_t)((blockIdx.x + k * gridDim.x) & 1u) << 3;  // cmode 2: tile's half of each row
@@ -288,7 +312,7 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
     // Loads are unconditional (a skipped TMA leaves stale data that is overwritten
     // below): no branch around the register tile, hence no phi-moves of it.
     if constexpr (NV == 1) {
-      issue(k + 2);
+      if constexpr (GR == 1) issue(k + 2);
       wait_seq(k);
       xs_addr = ring_s + (uint32_t)(k % kRing) * kSlotBytes;
       const uint32_t p0 = xs_addr + lb * 16u;  // natural (TMA) layout
@@ -404,14 +428,14 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
       for (int b = 0; b < W; ++b) local = local && Q.warps[b] == P.warps[b];
       const uint32_t nlb = lbase<W>(P, lane, warp);
       const uint32_t so = swz(lb) * 16u, sn = swz(nlb) * 16u;
-      if (local) __syncwarp(); else __syncthreads();
+      if (local) __syncwarp(); else gsync();
 #pragma unroll
       for (int q = 0; q < decltype(nvx)::value; ++q) {
         const uint32_t xa = q == 0 ? xs_addr : xb_addr;
 #pragma unroll
         for (int j = 0; j < NR; ++j) sts(xa + (so ^ (swz((uint32_t)j << Q.reg_l) * 16u)), v[q][j]);
       }
-      if (local) __syncwarp(); else __syncthreads();
+      if (local) __syncwarp(); else gsync();
 #pragma unroll
       for (int q = 0; q < decltype(nvx)::value; ++q) {
         const uint32_t xa = q == 0 ? xs_addr : xb_addr;
@@ -538,7 +562,10 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
         for (int j = 0; j < NR; ++j) st_stream(dst + gofs<IS_A>((uint32_t)j << RL, glo), v[q][j]);
       }
     }
-    if constexpr (NV == 1) __syncthreads();  // the slot may be refilled from the next iteration on
+    if constexpr (NV == 1) {
+      gsync();  // the slot may be refilled from here on
+      if constexpr (GR == 2) issue(k + 3);
+    }
   }
 
   // ------------------------------------------------------------ partial sums
@@ -549,12 +576,13 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
     acc1 = warp_sum(acc1 + acc1b);
     acc2 = warp_sum(acc2);
     acc3 = warp_sum(acc3);
-    constexpr int NW = 1 << W;
+    constexpr int NW = GR << W;
+    const int gw = threadIdx.x >> 5;
     if (lane == 0) {
-      red[warp] = acc0;
-      red[NW + warp] = acc1;
-      red[2 * NW + warp] = acc2;
-      red[3 * NW + warp] = acc3;
+      red[gw] = acc0;
+      red[NW + gw] = acc1;
+      red[2 * NW + gw] = acc2;
+      red[3 * NW + gw] = acc3;
     }
     __syncthreads();
     if (threadIdx.x < kSlots) {
@@ -568,16 +596,17 @@ __global__ void __launch_bounds__(32 << shape_w(SH), 1) k_sweep(const __grid_con
   }
 }
 
-template <int SH, int NV, int FORM, bool KSIN, bool FULL, int MODE = SM_PLAIN, int FORM2 = FORM>
+template <int SH, int NV, int FORM, bool KSIN, bool FULL, int MODE = SM_PLAIN, int FORM2 = FORM, int GR = 1,
+          uint32_t FM = 0xffffffffu>
 struct SweepKernel {
-  static constexpr int threads = 32 << shape_w(SH);
+  static constexpr int threads = GR * (32 << shape_w(SH));
   static int grid(qsb_ctx* ctx, uint64_t ntiles, unsigned* g) {
     static int occ = -1;  // per process; one device type
     if (occ < 0) {
-      QSB_CUDA(cudaFuncSetAttribute(k_sweep<SH, NV, FORM, KSIN, FULL, MODE, FORM2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      QSB_CUDA(cudaFuncSetAttribute(k_sweep<SH, NV, FORM, KSIN, FULL, MODE, FORM2, GR, FM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)kSmemBytes));
       int o = 0;
-      QSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sweep<SH, NV, FORM, KSIN, FULL, MODE, FORM2>, threads, kSmemBytes));
+      QSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sweep<SH, NV, FORM, KSIN, FULL, MODE, FORM2, GR, FM>, threads, kSmemBytes));
       occ = o < 1 ? 1 : o;
     }
     const uint64_t want = (uint64_t)ctx->num_sms * occ;
@@ -587,54 +616,69 @@ struct SweepKernel {
   static int launch(qsb_ctx* ctx, SweepArgs& a, unsigned* gout) {
     unsigned g;
     QSB_TRY(grid(ctx, a.ntiles, &g));
-    k_sweep<SH, NV, FORM, KSIN, FULL, MODE, FORM2><<<g, threads, kSmemBytes, ctx->stream>>>(a);
+    k_sweep<SH, NV, FORM, KSIN, FULL, MODE, FORM2, GR, FM><<<g, threads, kSmemBytes, ctx->stream>>>(a);
     QSB_CHECK_LAUNCH(ctx, "sweep");
     if (gout) *gout = g;
     return QSB_OK;
   }
 };
 
-// fast-mode instantiations of one register family (A shape SA, B shape SB).  A
-// sweeps always cover their whole 12-bit window; B windows may be partial (FULL=0).
-template <int NV, int SA, int SB>
+// fast-mode instantiations of one register family (A shape SA, B shape SB, GR warp
+// groups).  A sweeps always cover their whole 12-bit window; B windows may be partial.
+template <int NV, int SA, int SB, int GR = 1>
 int launch_fast(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
   auto L = [&](auto k) { return decltype(k)::launch(ctx, a, g); };
   const bool ksin = a.kind == 0;
   const bool c = a.form == GF_FACT_C;
+  constexpr int C = GF_FACT_C, S = GF_FACT_S, P = SM_PLAIN;
+  // lean instantiation: whole window, gates only (NV=2: + xsum) -- the chain's
+  // mid-layer sweeps
+  constexpr uint32_t LEAN = SF_POST_SCALE | (NV == 2 ? (uint32_t)SF_XSUM : 0u);
+  if (a.full && (a.flags & ~LEAN) == 0) {
+    if (a.shape == SA) return c ? L(SweepKernel<SA, NV, C, false, true, P, C, GR, LEAN>{})
+                                : L(SweepKernel<SA, NV, S, false, true, P, S, GR, LEAN>{});
+    return c ? L(SweepKernel<SB, NV, C, false, true, P, C, GR, LEAN>{})
+             : L(SweepKernel<SB, NV, S, false, true, P, S, GR, LEAN>{});
+  }
   if (a.shape == SA) {
     if (!a.full) {  // partial A windows (sharded tails below bit 12): runtime masks
-      if (c) return ksin ? L(SweepKernel<SA, NV, GF_FACT_C, true, false>{}) : L(SweepKernel<SA, NV, GF_FACT_C, false, false>{});
-      return ksin ? L(SweepKernel<SA, NV, GF_FACT_S, true, false>{}) : L(SweepKernel<SA, NV, GF_FACT_S, false, false>{});
+      if (c) return ksin ? L(SweepKernel<SA, NV, C, true, false, P, C, GR>{}) : L(SweepKernel<SA, NV, C, false, false, P, C, GR>{});
+      return ksin ? L(SweepKernel<SA, NV, S, true, false, P, S, GR>{}) : L(SweepKernel<SA, NV, S, false, false, P, S, GR>{});
     }
-    if (c) return ksin ? L(SweepKernel<SA, NV, GF_FACT_C, true, true>{}) : L(SweepKernel<SA, NV, GF_FACT_C, false, true>{});
-    return ksin ? L(SweepKernel<SA, NV, GF_FACT_S, true, true>{}) : L(SweepKernel<SA, NV, GF_FACT_S, false, true>{});
+    if (c) return ksin ? L(SweepKernel<SA, NV, C, true, true, P, C, GR>{}) : L(SweepKernel<SA, NV, C, false, true, P, C, GR>{});
+    return ksin ? L(SweepKernel<SA, NV, S, true, true, P, S, GR>{}) : L(SweepKernel<SA, NV, S, false, true, P, S, GR>{});
   }
-  if (a.full) return c ? L(SweepKernel<SB, NV, GF_FACT_C, false, true>{}) : L(SweepKernel<SB, NV, GF_FACT_S, false, true>{});
-  return c ? L(SweepKernel<SB, NV, GF_FACT_C, false, false>{}) : L(SweepKernel<SB, NV, GF_FACT_S, false, false>{});
+  if (a.full) return c ? L(SweepKernel<SB, NV, C, false, true, P, C, GR>{}) : L(SweepKernel<SB, NV, S, false, true, P, S, GR>{});
+  return c ? L(SweepKernel<SB, NV, C, false, false, P, C, GR>{}) : L(SweepKernel<SB, NV, S, false, false, P, S, GR>{});
 }
 
 // merged / bridge instantiations (fast mode; shapes SA / SB of one register family).  Table ops between
 // the passes dispatch on the table kind at run time (KSIN = false).
-template <int NV, int MODE, int F1, int SA = SH_A2, int SB = SH_B2>
+template <int NV, int MODE, int F1, int SA = SH_A2, int SB = SH_B2, int GR = 1>
 int launch_merged_f1(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
   auto L = [&](auto k) { return decltype(k)::launch(ctx, a, g); };
+  // every flag a merged / bridge sweep of this kind can carry (run_chain, fused.cu)
+  constexpr uint32_t M = SF_POST_SCALE | (MODE == SM_BRIDGE ? (uint32_t)(SF_MID_EXPECT | SF_XSUM2)
+                                          : NV == 1 ? (uint32_t)SF_MID_PHASE
+                                                    : (uint32_t)(SF_XSUM | SF_MID_DINNER | SF_MID_PHASE | SF_XSUM2));
+  if ((a.flags & ~M) != 0) return invalid("internal: unexpected flags 0x%x for a merged sweep", a.flags);
   const bool c2 = a.form2 == GF_FACT_C;
   if constexpr (MODE == SM_BRIDGE) {  // Rx(-2b) then Rx(+2b): the same form
-    if (a.shape == SA) return a.full ? L(SweepKernel<SA, NV, F1, false, true, MODE, F1>{})
-                                        : L(SweepKernel<SA, NV, F1, false, false, MODE, F1>{});
-    return a.full ? L(SweepKernel<SB, NV, F1, false, true, MODE, F1>{})
-                  : L(SweepKernel<SB, NV, F1, false, false, MODE, F1>{});
+    if (a.shape == SA) return a.full ? L(SweepKernel<SA, NV, F1, false, true, MODE, F1, GR, M>{})
+                                        : L(SweepKernel<SA, NV, F1, false, false, MODE, F1, GR, M>{});
+    return a.full ? L(SweepKernel<SB, NV, F1, false, true, MODE, F1, GR, M>{})
+                  : L(SweepKernel<SB, NV, F1, false, false, MODE, F1, GR, M>{});
   } else {
     if (a.shape == SA) {
-      if (a.full) return c2 ? L(SweepKernel<SA, NV, F1, false, true, MODE, GF_FACT_C>{})
-                            : L(SweepKernel<SA, NV, F1, false, true, MODE, GF_FACT_S>{});
-      return c2 ? L(SweepKernel<SA, NV, F1, false, false, MODE, GF_FACT_C>{})
-                : L(SweepKernel<SA, NV, F1, false, false, MODE, GF_FACT_S>{});
+      if (a.full) return c2 ? L(SweepKernel<SA, NV, F1, false, true, MODE, GF_FACT_C, GR, M>{})
+                            : L(SweepKernel<SA, NV, F1, false, true, MODE, GF_FACT_S, GR, M>{});
+      return c2 ? L(SweepKernel<SA, NV, F1, false, false, MODE, GF_FACT_C, GR, M>{})
+                : L(SweepKernel<SA, NV, F1, false, false, MODE, GF_FACT_S, GR, M>{});
     }
-    if (a.full) return c2 ? L(SweepKernel<SB, NV, F1, false, true, MODE, GF_FACT_C>{})
-                          : L(SweepKernel<SB, NV, F1, false, true, MODE, GF_FACT_S>{});
-    return c2 ? L(SweepKernel<SB, NV, F1, false, false, MODE, GF_FACT_C>{})
-              : L(SweepKernel<SB, NV, F1, false, false, MODE, GF_FACT_S>{});
+    if (a.full) return c2 ? L(SweepKernel<SB, NV, F1, false, true, MODE, GF_FACT_C, GR, M>{})
+                          : L(SweepKernel<SB, NV, F1, false, true, MODE, GF_FACT_S, GR, M>{});
+    return c2 ? L(SweepKernel<SB, NV, F1, false, false, MODE, GF_FACT_C, GR, M>{})
+              : L(SweepKernel<SB, NV, F1, false, false, MODE, GF_FACT_S, GR, M>{});
   }
 }
 

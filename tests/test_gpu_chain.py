@@ -91,14 +91,17 @@ def test_chain_float_table(monkeypatch):
     assert rel_err(psi, want_psi) <= 1e-10
 
 
+@pytest.mark.parametrize("fam", ["5", "6"])
 @pytest.mark.parametrize("n,p", [(21, 2), (27, 2), (30, 2)])
-def test_chain_register_families(n, p, monkeypatch):
-    """merged single-vector sweeps with 32 amplitudes per thread (R=5: B windows need
-    one exchange per pass) against the default R=4 family"""
+def test_chain_register_families(n, p, fam, monkeypatch):
+    """single-vector sweeps with 32 amplitudes per thread (R=5: B windows need one
+    exchange per pass; family 6 = two independent warp groups per CTA) against the
+    default R=4 family"""
     poly = random_instance(300 + n, n)
     params = params_wide(11 * n + p, p)
     ref = run(poly, params, monkeypatch, merge=True)
-    monkeypatch.setenv("QSB_SWEEP_R1M", "5")
+    monkeypatch.setenv("QSB_SWEEP_R1M", fam)
+    monkeypatch.setenv("QSB_SWEEP_R1", fam)
     got = run(poly, params, monkeypatch, merge=True)
     assert abs(got[0] - ref[0]) <= 1e-12 * max(1.0, abs(ref[0]))
     assert rel_err(got[1], ref[1]) <= 1e-12

@@ -1,0 +1,305 @@
+// Streaming-structure probe (not part of the library): how fast can a persistent
+// one-CTA-per-SM kernel stream a 16 GiB complex128 array HBM -> smem -> registers ->
+// HBM with the sweep kernel's data movement, without the gate arithmetic?
+//   mode 0: TMA 1-D tile load (3-slot ring) -> LDS -> STG            (the sweep's I/O)
+//   mode 1: mode 0 + 2 swizzled smem exchanges per tile               (+ sweep's smem)
+//   mode 2: TMA load -> LDS -> STS back into the slot -> TMA 1-D store (bulk store)
+//   mode 3: plain LDG.128 -> STG.128 grid-stride copy                 (no smem)
+//   mode 5/6: B tile (global bits 0..2 + 9 bits at glo = 12 / 21) via a 5-D TMA box,
+//           strided STG, no arithmetic                                (B-sweep I/O)
+//   mode 4: the sweep's A-window work: 3 phase maps, 2 exchanges, 4 gate levels each
+//           (factored Rx butterflies, 4 DFMA per pair), post scale     (= k_sweep NV=1)
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o probe tools/probe_stream.cu
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+constexpr int kT = 12, kTile = 1 << kT, kSlot = kTile * 16, kRing = 3;
+
+__device__ __forceinline__ double2 lds(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts(uint32_t a, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void stg(double2* p, double2 v) {
+  asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra W_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__host__ __device__ constexpr uint32_t swz(uint32_t x) { return x ^ (((x >> 3) ^ (x >> 6) ^ (x >> 9) ^ (x >> 12)) & 7u); }
+
+struct Map {
+  int lanes[5], warps[3], reg;
+};
+__host__ __device__ constexpr Map map_of(int p) {
+  return p == 0 ? Map{{0, 1, 2, 3, 4}, {5, 6, 7}, 8} : p == 1 ? Map{{4, 5, 6, 7, 8}, {9, 10, 11}, 0} : Map{{0, 1, 2, 3, 8}, {9, 10, 11}, 4};
+}
+__device__ __forceinline__ uint32_t mbase(const Map& m, int lane, int warp) {
+  uint32_t l = 0;
+#pragma unroll
+  for (int b = 0; b < 5; ++b) l |= (uint32_t)((lane >> b) & 1) << m.lanes[b];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) l |= (uint32_t)((warp >> b) & 1) << m.warps[b];
+  return l;
+}
+__device__ __forceinline__ void bfly(double2& t, double2& u, double gb) {
+  const double2 n0 = make_double2(fma(gb, u.y, t.x), fma(-gb, u.x, t.y));
+  const double2 n1 = make_double2(fma(gb, t.y, u.x), fma(-gb, t.x, u.y));
+  t = n0;
+  u = n1;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 1) k_stream(const double2* __restrict__ src, double2* __restrict__ dst,
+                                                    uint64_t ntiles, double scale) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t bars = ring + kRing * kSlot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < kRing; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bars + 8 * s));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto issue = [&](uint64_t k) {
+    if (tid != 0 || k >= mine) return;
+    const uint64_t t = blockIdx.x + k * gridDim.x;
+    const uint32_t slot = (uint32_t)(k % kRing), bar = bars + 8 * slot;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kSlot) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     ring + slot * kSlot),
+                 "l"(src + (t << kT)), "r"(kSlot), "r"(bar)
+                 : "memory");
+  };
+  issue(0);
+  issue(1);
+  for (uint64_t k = 0; k < mine; ++k) {
+    const uint64_t t = blockIdx.x + k * gridDim.x;
+    if (MODE != 2) issue(k + 2);
+    mbar_wait(bars + 8 * (uint32_t)(k % kRing), (uint32_t)((k / kRing) & 1));
+    const uint32_t slot = ring + (uint32_t)(k % kRing) * kSlot;
+    // natural map: lanes = bits 0..4, warps = bits 5..7, registers = bits 8..11
+    const uint32_t lb = (uint32_t)lane | ((uint32_t)warp << 5);
+    double2 v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = lds(slot + (lb | (j << 8)) * 16u);
+    if (MODE == 1) {
+      // two exchanges: regs <-> bits 0..3, then back (same traffic as the sweep's)
+      const uint32_t lb1 = ((uint32_t)lane << 4) | ((uint32_t)(warp & 1) << 9) | ((uint32_t)(warp >> 1) << 10);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const uint32_t a0 = e == 0 ? lb : lb1, a1 = e == 0 ? lb1 : lb;
+        const int r0 = e == 0 ? 8 : 0, r1 = e == 0 ? 0 : 8;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sts(slot + swz(a0 | (j << r0)) * 16u, v[j]);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = lds(slot + swz(a1 | (j << r1)) * 16u);
+      }
+    }
+    uint32_t lout = lb;
+    int rout = 8;
+    if (MODE == 4) {
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        const Map P = map_of(p);
+        if (p > 0) {
+          const Map Q = map_of(p - 1);
+          const uint32_t qb = mbase(Q, lane, warp), pb = mbase(P, lane, warp);
+          __syncthreads();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) sts(slot + swz(qb | (j << Q.reg)) * 16u, v[j]);
+          __syncthreads();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = lds(slot + swz(pb | (j << P.reg)) * 16u);
+        }
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (!(j & (1 << b))) bfly(v[j], v[j | (1 << b)], scale * 0.25);
+      }
+      lout = mbase(map_of(2), lane, warp);
+      rout = 4;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = make_double2(v[j].x * scale, v[j].y * scale);
+    if (MODE == 2) {
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) sts(slot + (lb | (j << 8)) * 16u, v[j]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + (t << kT)), "r"(slot),
+                     "r"(kSlot)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        // the slot is refilled two tiles later: allow one store group in flight
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      }
+      __syncthreads();
+      issue(k + 2);  // into slot (k+2)%3 == (k-1)%3, whose store was waited for above
+    } else {
+      double2* d = dst + (t << kT);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 16; ++j) stg(d + (lout | (j << rout)), v[j]);
+      __syncthreads();
+    }
+  }
+  if (MODE == 2 && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// B tile with L contiguous low bits (runs of 2^L amplitudes) and 12-L window bits at
+// glo; SC: store contiguous (tile order) instead of back to the strided positions
+template <int L, bool SC>
+__global__ void __launch_bounds__(256, 1) k_btile(const __grid_constant__ CUtensorMap tm, double2* __restrict__ dst,
+                                                  uint64_t ntiles, int glo, double scale) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t bars = ring + kRing * kSlot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < kRing; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bars + 8 * s));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int lowbits = glo - L;
+  auto issue = [&](uint64_t k) {
+    if (tid != 0 || k >= mine) return;
+    const uint64_t t = blockIdx.x + k * gridDim.x;
+    const uint32_t slot = (uint32_t)(k % kRing), bar = bars + 8 * slot;
+    const int c1 = (int)(t & ((1ull << lowbits) - 1)), c4 = (int)(t >> lowbits);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kSlot) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+        "%6}], [%7];" ::"r"(ring + slot * kSlot),
+        "l"(&tm), "r"(0), "r"(c1), "r"(0), "r"(0), "r"(c4), "r"(bar)
+        : "memory");
+  };
+  issue(0);
+  issue(1);
+  for (uint64_t k = 0; k < mine; ++k) {
+    const uint64_t t = blockIdx.x + k * gridDim.x;
+    issue(k + 2);
+    mbar_wait(bars + 8 * (uint32_t)(k % kRing), (uint32_t)((k / kRing) & 1));
+    const uint32_t slot = ring + (uint32_t)(k % kRing) * kSlot;
+    const uint32_t lb = (uint32_t)lane | ((uint32_t)warp << 5);
+    double2 v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = lds(slot + (lb | (j << 8)) * 16u);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = make_double2(v[j].x * scale, v[j].y * scale);
+    const uint64_t base = (t & ((1ull << lowbits) - 1)) << L | (t >> lowbits) << (glo + 12 - L);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t l = lb | (j << 8);
+      if (SC) stg(dst + ((t << kT) | l), v[j]);
+      else stg(dst + (base | (l & ((1u << L) - 1)) | ((uint64_t)(l >> L) << glo)), v[j]);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_ldg(const double2* __restrict__ src, double2* __restrict__ dst, uint64_t n, double scale) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    double2 v = __ldcs(src + i);
+    __stcs(dst + i, make_double2(v.x * scale, v.y * scale));
+  }
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                            const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                            CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static CUtensorMap bmap(const double2* base, int n, int glo, int L,
+                        CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+  CUtensorMap m;
+  const int H = 12 - L;  // window bits: 5 + (H - 5)
+  const cuuint64_t dims[5] = {2ull << L, 1ull << (glo - L), 32, 1ull << (H - 5), 1ull << (n - glo - H)};
+  const cuuint64_t strides[4] = {(1ull << L) * 16, (1ull << glo) * 16, (1ull << (glo + 5)) * 16, (1ull << (glo + H)) * 16};
+  const cuuint32_t box[5] = {2u << L, 1, 32, 1u << (H - 5), 1};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = ((EncodeFn)p)(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)base, dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r) printf("encode failed %d (L=%d glo=%d)\n", (int)r, L, glo);
+  return m;
+}
+
+int main() {
+  const int n = 30;
+  const uint64_t N = 1ull << n;
+  double2 *a, *b;
+  if (cudaMalloc(&a, N * 16) || cudaMalloc(&b, N * 16)) {
+    printf("alloc failed\n");
+    return 1;
+  }
+  cudaMemset(a, 0x3f, N * 16);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const size_t smem = kRing * kSlot + 64;
+  cudaFuncSetAttribute(k_stream<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_stream<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_stream<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_stream<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_btile<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_btile<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_btile<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_btile<5, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_btile<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const CUtensorMap m12 = bmap(a, n, 12, 3), m21 = bmap(a, n, 21, 3), m4 = bmap(a, n, 18, 4), m5 = bmap(a, n, 18, 5),
+                    m2 = bmap(a, n, 18, 2);
+  const CUtensorMap mp0 = bmap(a, n, 21, 3, CU_TENSOR_MAP_L2_PROMOTION_NONE),
+                    mp1 = bmap(a, n, 21, 3, CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const uint64_t ntiles = N >> kT;
+  const char* names[] = {"tma1d+stg", "tma1d+2exch+stg", "tma1d+tma-store", "ldg/stg", "A-window full sweep work",
+                         "B L=3 glo=12", "B L=3 glo=21", "B L=3 glo=21, contiguous store", "B L=4 glo=18",
+                         "B L=5 glo=18", "B L=2 glo=18", "B L=3 glo=21 promo none", "B L=3 glo=21 promo 128",
+                         "B L=3 glo=21 2x grid (2 CTA/SM? no)"};
+  for (int mode = 0; mode < 13; ++mode) {
+    float best = 1e9f;
+    for (int rep = 0; rep < 5; ++rep) {
+      cudaEventRecord(e0);
+      if (mode == 0) k_stream<0><<<sms, 256, smem>>>(a, b, ntiles, 1.0);
+      if (mode == 1) k_stream<1><<<sms, 256, smem>>>(a, b, ntiles, 1.0);
+      if (mode == 2) k_stream<2><<<sms, 256, smem>>>(a, b, ntiles, 1.0);
+      if (mode == 3) k_ldg<<<sms * 8, 256>>>(a, b, N, 1.0);
+      if (mode == 4) k_stream<4><<<sms, 256, smem>>>(a, b, ntiles, 1.0);
+      if (mode == 5) k_btile<3, false><<<sms, 256, smem>>>(m12, b, ntiles, 12, 1.0);
+      if (mode == 6) k_btile<3, false><<<sms, 256, smem>>>(m21, b, ntiles, 21, 1.0);
+      if (mode == 7) k_btile<3, true><<<sms, 256, smem>>>(m21, b, ntiles, 21, 1.0);
+      if (mode == 8) k_btile<4, false><<<sms, 256, smem>>>(m4, b, ntiles, 18, 1.0);
+      if (mode == 9) k_btile<5, false><<<sms, 256, smem>>>(m5, b, ntiles, 18, 1.0);
+      if (mode == 10) k_btile<2, false><<<sms, 256, smem>>>(m2, b, ntiles, 18, 1.0);
+      if (mode == 11) k_btile<3, false><<<sms, 256, smem>>>(mp0, b, ntiles, 21, 1.0);
+      if (mode == 12) k_btile<3, false><<<sms, 256, smem>>>(mp1, b, ntiles, 21, 1.0);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (ms < best) best = ms;
+    }
+    cudaError_t err = cudaGetLastError();
+    printf("mode %d %-34s: %.3f ms  %.1f GB/s  (%s)\n", mode, names[mode], best, 32.0 * N / (best * 1e-3) / 1e9, cudaGetErrorString(err));
+  }
+  return 0;
+}
