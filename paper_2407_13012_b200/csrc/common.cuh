@@ -49,6 +49,10 @@ struct qsb_ctx {
   // reusable device scratch for reduction partials (grown on demand)
   double* d_scratch = nullptr;
   uint64_t scratch_bytes = 0;
+  // sampler scratch (probability-tree levels k0..n + shot outputs), grown on demand and
+  // kept: re-allocating ~0.5 GB per draw costs more than the draw itself
+  void* d_sample = nullptr;
+  uint64_t sample_bytes = 0;
   // pinned host staging for small results
   double* h_small = nullptr;  // 4096 doubles
   // reusable device buffer for small uploads (LUTs, terms)
@@ -84,6 +88,7 @@ namespace qsb {
 int prof_mark(qsb_ctx* ctx, cudaEvent_t* ev);
 int ensure_scratch(qsb_ctx* ctx, uint64_t bytes);
 int ensure_small(qsb_ctx* ctx, uint64_t bytes);
+int ensure_sample_scratch(qsb_ctx* ctx, uint64_t bytes);
 // build (cos, sin) of (sign * gamma * v) for v = vmin + k, k < nvals, with host libm
 // (the same values Python's math.cos/sin and numba give) and upload to t->d_lut.
 int upload_phase_lut(qsb_table* t, double ang_scale, double2 extra_scale, bool exact);

@@ -48,6 +48,24 @@ int ensure_scratch(qsb_ctx* ctx, uint64_t bytes) {
   return QSB_OK;
 }
 
+int ensure_sample_scratch(qsb_ctx* ctx, uint64_t bytes) {
+  if (bytes <= ctx->sample_bytes) return QSB_OK;
+  if (ctx->d_sample) {
+    QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    QSB_CUDA(cudaFree(ctx->d_sample));
+    ctx->d_sample = nullptr;
+    ctx->sample_bytes = 0;
+  }
+  cudaError_t e = cudaMalloc(&ctx->d_sample, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return ::qsb::cuda_fail(e, "sampler scratch");
+  }
+  QSB_CUDA(e);
+  ctx->sample_bytes = bytes;
+  return QSB_OK;
+}
+
 int ensure_small(qsb_ctx* ctx, uint64_t bytes) {
   if (bytes <= ctx->small_bytes) return QSB_OK;
   if (ctx->d_small) {
@@ -123,6 +141,7 @@ int qsb_ctx_destroy(qsb_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->d_scratch) cudaFree(ctx->d_scratch);
   if (ctx->d_small) cudaFree(ctx->d_small);
+  if (ctx->d_sample) cudaFree(ctx->d_sample);
   if (ctx->h_small) cudaFreeHost(ctx->h_small);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);

@@ -4,11 +4,12 @@
 // The reference builds every pairwise level of the probability tree
 // (leaves |psi_i|^2, level l+1 = src[2i] + src[2i+1]) and descends it once per
 // shot with a splitmix64 uniform scaled by the root.  The GPU builds the same
-// levels 1..n with the same association (11 levels per launch: 3 in registers,
-// 5 by warp shuffle, 3 through shared memory), never stores the leaves (they are
-// recomputed from two amplitudes at the bottom of the descent), then runs one
-// thread per shot.  Every floating-point operation matches the reference, so
-// given the same state the drawn indices are bit-identical.
+// levels with the same association (11 levels per launch: 3 in registers, 5 by
+// warp shuffle, 3 through shared memory) but stores only levels k0..n (k0 = 5:
+// 1/16 of the tree, 512 MB at n=30); one thread per shot descends the stored
+// levels, then rebuilds its 32-leaf subtree from the amplitudes (the same adds in
+// the same order) for the last k0 steps.  Every floating-point operation matches
+// the reference, so given the same state the drawn indices are bit-identical.
 #include <math.h>
 
 #include "common.cuh"
@@ -22,12 +23,18 @@ constexpr int kBT = 256;        // threads per build block
 constexpr int kBPer = 8;        // inputs per thread
 constexpr int kBIn = kBT * kBPer;  // 2048 inputs per block -> 11 levels
 
+constexpr int kK0 = 5;  // lowest stored level (below: rebuilt per shot from 2^k0 leaves)
+
 struct Levels {
   double* base;
   uint64_t N;
   int n;
-  // level l >= 1 starts at sum_{k=1}^{l-1} N >> k = N - (N >> (l-1)); the root is at N - 2
-  __host__ __device__ uint64_t off(int l) const { return N - (N >> (l - 1)); }
+  int k0;  // min(kK0, n)
+  // level l >= k0 starts at sum_{k=k0}^{l-1} N >> k = (N >> (k0-1)) - (N >> (l-1))
+  __host__ __device__ uint64_t off(int l) const { return (N >> (k0 - 1)) - (N >> (l - 1)); }
+  __host__ __device__ bool stored(int l) const { return l >= k0 && l <= n; }
+  // entries of levels k0..n
+  __host__ __device__ uint64_t count() const { return (N >> (k0 - 1)) - (N >> n); }
 };
 
 // Build levels l0+1 .. l0+11 (those <= n) from level l0 (l0 == 0: from amplitudes).
@@ -50,7 +57,7 @@ __global__ void __launch_bounds__(kBT) k_build(const double2* __restrict__ amps,
 #pragma unroll
     for (int e = 0; e < w; ++e) r[e] = __dadd_rn(r[2 * e], r[2 * e + 1]);
     const int l = l0 + k;
-    if (l <= L.n) {
+    if (L.stored(l)) {
       const uint64_t cnt = L.N >> l;
       double* dst = L.base + L.off(l);
       const uint64_t j0 = (i0 >> k);
@@ -67,7 +74,7 @@ __global__ void __launch_bounds__(kBT) k_build(const double2* __restrict__ amps,
   for (int k = 0; k < 5; ++k) {
     v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, 1 << k));
     const int l = lvl + 1 + k;
-    if (l <= L.n && (lane & ((2 << k) - 1)) == 0) {
+    if (L.stored(l) && (lane & ((2 << k) - 1)) == 0) {
       const uint64_t cnt = L.N >> l;
       const uint64_t j = (i0 >> 3) >> (k + 1);
       if (j < cnt) L.base[L.off(l) + j] = v;
@@ -86,7 +93,7 @@ __global__ void __launch_bounds__(kBT) k_build(const double2* __restrict__ amps,
 #pragma unroll
       for (int e = 0; e < w; ++e) w8[e] = __dadd_rn(w8[2 * e], w8[2 * e + 1]);
       const int l = lvl + 1 + k;
-      if (l <= L.n) {
+      if (L.stored(l)) {
         const uint64_t cnt = L.N >> l;
         const uint64_t j0 = (uint64_t)blockIdx.x * w;
         for (int e = 0; e < w; ++e)
@@ -108,18 +115,43 @@ __global__ void k_descend(const double2* __restrict__ amps, Levels L, const doub
     // rng.uniform_block(seed, 0, shots)[s] * total  (rng.py:40-47, backend.py:291)
     const uint64_t z = mix64(seed + (s + 1) * 0x9E3779B97F4A7C15ull);
     double u = __dmul_rn(__dmul_rn((double)(z >> 11), 0x1.0p-53), root);
-    uint64_t idx = 0;
-    for (int l = L.n - 1; l >= 1; --l) {
+    uint64_t idx = 0;  // node at level l+1
+    for (int l = L.n - 1; l >= L.k0; --l) {
       const double left = L.base[L.off(l) + 2 * idx];
       const bool right = u >= left;
       if (right) u = __dadd_rn(u, -left);
       idx = 2 * idx + (right ? 1 : 0);
     }
-    {
-      const double left = norm2_exact(amps[2 * idx]);
-      const bool right = u >= left;
-      idx = 2 * idx + (right ? 1 : 0);
+    // idx is a node of level k0: rebuild its subtree (levels 0..k0-1) from the
+    // 2^k0 amplitudes below it, exactly as the reference's levels were formed
+    double t[2 << kK0];  // t[0..2^k0) leaves, then level 1, level 2, ... packed
+    const int k0 = L.k0;
+    const uint64_t leaf0 = idx << k0;
+#pragma unroll
+    for (int e = 0; e < (1 << kK0); ++e)
+      if (e < (1 << k0)) t[e] = norm2_exact(amps[leaf0 + e]);
+    int lo[kK0 + 1];
+    lo[0] = 0;
+#pragma unroll
+    for (int l = 1; l <= kK0; ++l) {
+      lo[l] = lo[l - 1] + (1 << (kK0 - l + 1));
+      if (l < k0) {
+#pragma unroll
+        for (int e = 0; e < (1 << (kK0 - l)); ++e)
+          if (e < (1 << (k0 - l))) t[lo[l] + e] = __dadd_rn(t[lo[l - 1] + 2 * e], t[lo[l - 1] + 2 * e + 1]);
+      }
     }
+    uint64_t loc = 0;  // node within the subtree at level l+1
+#pragma unroll
+    for (int l = kK0 - 1; l >= 0; --l) {
+      if (l < k0) {
+        const double left = t[lo[l] + 2 * loc];
+        const bool right = u >= left;
+        if (right && l > 0) u = __dadd_rn(u, -left);
+        loc = 2 * loc + (right ? 1 : 0);
+      }
+    }
+    idx = leaf0 + loc;
     idx_out[s] = (int64_t)idx;
     if (table) cost_out[s] = table[idx];
   }
@@ -139,12 +171,15 @@ int qsb_sample(qsb_ctx* ctx, qsb_table* t, const double* amps, int n, uint64_t s
   const uint64_t N = 1ull << n;
   const double2* a = (const double2*)amps;
   double root;
-  double* levels = nullptr;
-  int64_t* d_idx = nullptr;
-  double* d_cost = nullptr;
-  const uint64_t lv_count = N > 1 ? N - 1 : 1;
-  QSB_CUDA(cudaMallocAsync((void**)&levels, lv_count * sizeof(double), ctx->stream));
-  Levels L{levels, N, n};
+  const int k0 = n < kK0 ? n : kK0;
+  Levels L{nullptr, N, n, k0};
+  // scratch: levels k0..n, then the shot outputs (indices, costs)
+  const uint64_t lv_bytes = (L.count() * sizeof(double) + 255) & ~255ull;
+  QSB_TRY(ensure_sample_scratch(ctx, lv_bytes + shots * (sizeof(int64_t) + sizeof(double))));
+  double* levels = (double*)ctx->d_sample;
+  int64_t* d_idx = (int64_t*)((char*)ctx->d_sample + lv_bytes);
+  double* d_cost = t ? (double*)(d_idx + shots) : nullptr;
+  L.base = levels;
   int rc = QSB_OK;
   for (int l0 = 0; l0 < n; l0 += 11) {
     const uint64_t M = N >> l0;
@@ -165,11 +200,6 @@ int qsb_sample(qsb_ctx* ctx, qsb_table* t, const double* amps, int n, uint64_t s
     if (!(fabs(root - 1.0) <= 1e-9)) rc = invalid("state is not normalized: sum of probabilities = %.17g", root);
   }
   if (rc == QSB_OK) {
-    e = cudaMallocAsync((void**)&d_idx, shots * sizeof(int64_t), ctx->stream);
-    if (e == cudaSuccess && t) e = cudaMallocAsync((void**)&d_cost, shots * sizeof(double), ctx->stream);
-    if (e != cudaSuccess) rc = cuda_fail(e, "sample output allocation");
-  }
-  if (rc == QSB_OK) {
     uint64_t blocks = (shots + 255) / 256;
     if (blocks > (uint64_t)ctx->num_sms * 64) blocks = (uint64_t)ctx->num_sms * 64;
     k_descend<<<(unsigned)blocks, 256, 0, ctx->stream>>>(a, L, t ? t->values : nullptr, shots, seed, root, d_idx, d_cost);
@@ -181,9 +211,6 @@ int qsb_sample(qsb_ctx* ctx, qsb_table* t, const double* amps, int n, uint64_t s
     if (e != cudaSuccess) rc = cuda_fail(e, "sample descent");
     ctx->d2h_bytes += shots * (sizeof(int64_t) + (t ? sizeof(double) : 0)) + sizeof(double);
   }
-  if (d_idx) cudaFreeAsync(d_idx, ctx->stream);
-  if (d_cost) cudaFreeAsync(d_cost, ctx->stream);
-  cudaFreeAsync(levels, ctx->stream);
   return rc;
 }
 

@@ -631,14 +631,16 @@ int launch_fast(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
   const bool ksin = a.kind == 0;
   const bool c = a.form == GF_FACT_C;
   constexpr int C = GF_FACT_C, S = GF_FACT_S, P = SM_PLAIN;
-  // lean instantiation: whole window, gates only (NV=2: + xsum) -- the chain's
-  // mid-layer sweeps
-  constexpr uint32_t LEAN = SF_POST_SCALE | (NV == 2 ? (uint32_t)SF_XSUM : 0u);
-  if (a.full && (a.flags & ~LEAN) == 0) {
-    if (a.shape == SA) return c ? L(SweepKernel<SA, NV, C, false, true, P, C, GR, LEAN>{})
-                                : L(SweepKernel<SA, NV, S, false, true, P, S, GR, LEAN>{});
-    return c ? L(SweepKernel<SB, NV, C, false, true, P, C, GR, LEAN>{})
-             : L(SweepKernel<SB, NV, S, false, true, P, S, GR, LEAN>{});
+  // lean instantiation: whole window, gates only -- the chain's mid-layer forward
+  // sweeps (for bra/ket sweeps the lean variant measured slower: not used)
+  constexpr uint32_t LEAN = SF_POST_SCALE;
+  if constexpr (NV == 1) {
+    if (a.full && (a.flags & ~LEAN) == 0) {
+      if (a.shape == SA) return c ? L(SweepKernel<SA, NV, C, false, true, P, C, GR, LEAN>{})
+                                  : L(SweepKernel<SA, NV, S, false, true, P, S, GR, LEAN>{});
+      return c ? L(SweepKernel<SB, NV, C, false, true, P, C, GR, LEAN>{})
+               : L(SweepKernel<SB, NV, S, false, true, P, S, GR, LEAN>{});
+    }
   }
   if (a.shape == SA) {
     if (!a.full) {  // partial A windows (sharded tails below bit 12): runtime masks
