@@ -54,8 +54,13 @@ std::vector<SweepShape> plan_sweeps(int n) { return plan_range(n, 0, n - 1); }
 // QSB_SWEEP_R2 (plain sweeps, 3..6 / 3..4) and QSB_SWEEP_R1M (merged single-vector
 // sweeps, 4..6; merged bra/ket sweeps are R=4 only).  6 = the R=5 shapes with two
 // independent warp groups per CTA.
-int sweep_family(int nv, bool merged) {
-  if (merged && nv == 2) return 4;
+int sweep_family(int nv, int mode) {
+  const bool merged = mode != SM_PLAIN;
+  if (mode == SM_BRIDGE) return 4;
+  if (merged && nv == 2) {  // QSB_SWEEP_R2M: 3 (16 warps) or 4
+    const char* e2 = getenv("QSB_SWEEP_R2M");
+    return (e2 && atoi(e2) == 3) ? 3 : 4;
+  }
   const char* e = getenv(merged ? "QSB_SWEEP_R1M" : (nv == 1 ? "QSB_SWEEP_R1" : "QSB_SWEEP_R2"));
   int r = e ? atoi(e) : 4;
   if (merged) return (r == 5 || r == 6) ? r : 4;
@@ -66,10 +71,11 @@ int sweep_family(int nv, bool merged) {
 
 // Fill the tile/phase part of SweepArgs for one sweep. Returns the number of gates.
 int build_shape(const SweepShape& sh, int n, int nv, bool exact, SweepArgs& a, int gates_before_phase[kMaxPhases],
-                const int* pass2 = nullptr, int gates_before_phase2[kMaxPhases] = nullptr, int* gates2 = nullptr) {
+                const int* pass2 = nullptr, int gates_before_phase2[kMaxPhases] = nullptr, int* gates2 = nullptr,
+                int mode = SM_PLAIN) {
   int gl[kSweepT];
   for (int i = 0; i < kSweepT; ++i) gl[i] = sh.is_a ? i : (i < 3 ? i : sh.glo + i - 3);
-  const int fam = exact ? 4 : sweep_family(nv, pass2 != nullptr);
+  const int fam = exact ? 4 : sweep_family(nv, mode);
   const int shape = pick_shape(exact, sh.is_a, fam);
   a.groups = fam == 6 ? 2 : 1;
   const int np = shape_np(shape);
@@ -339,7 +345,7 @@ struct Runner {
     SweepArgs a;
     memset(&a, 0, sizeof(a));
     int gbp[kMaxPhases], gbp2[kMaxPhases] = {0, 0, 0, 0}, gates2 = 0;
-    const int gates = build_shape(sh, n, nv, exact, a, gbp, mode != SM_PLAIN ? pass2 : nullptr, gbp2, &gates2);
+    const int gates = build_shape(sh, n, nv, exact, a, gbp, mode != SM_PLAIN ? pass2 : nullptr, gbp2, &gates2, mode);
     if (gates < 0) return invalid("internal: bad sweep layout");
     a.mode = mode;
     a.v0 = v0;

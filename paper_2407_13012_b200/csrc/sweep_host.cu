@@ -22,13 +22,15 @@ int launch_sweep_nv1_r5g(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_m_nv2_c(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_m_nv2_s(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_bridge(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int launch_sweep_m_nv2_r3_c(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int launch_sweep_m_nv2_r3_s(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 
 int launch_sweep(qsb_ctx* ctx, int nv, bool exact, SweepArgs& a, unsigned* gout) {
   if (a.mode != SM_PLAIN) {
     const int r = shape_r(a.shape);
-    if (exact || a.form == GF_EXACT || a.shape != pick_shape(false, shape_is_a(a.shape), r) || r == 3 ||
-        (nv == 2 && r != 4))
-      return invalid("internal: merged sweeps are fast-mode; R=4 (NV=1/2) or R=5 (NV=1) shapes");
+    if (exact || a.form == GF_EXACT || a.shape != pick_shape(false, shape_is_a(a.shape), r) ||
+        (nv == 1 && r == 3) || (nv == 2 && r == 5) || (a.mode == SM_BRIDGE && r != 4))
+      return invalid("internal: merged sweeps are fast-mode; R=4 or R=5 (NV=1) / R=3 (NV=2) shapes");
     if (a.mode == SM_BRIDGE) return nv == 2 ? launch_sweep_bridge(ctx, a, gout) : invalid("internal: bridge needs nv=2");
     const bool c = a.form == GF_FACT_C;
     if (nv == 1) {
@@ -36,6 +38,7 @@ int launch_sweep(qsb_ctx* ctx, int nv, bool exact, SweepArgs& a, unsigned* gout)
       if (r == 5) return c ? launch_sweep_m_nv1_r5_c(ctx, a, gout) : launch_sweep_m_nv1_r5_s(ctx, a, gout);
       return c ? launch_sweep_m_nv1_r4_c(ctx, a, gout) : launch_sweep_m_nv1_r4_s(ctx, a, gout);
     }
+    if (r == 3) return c ? launch_sweep_m_nv2_r3_c(ctx, a, gout) : launch_sweep_m_nv2_r3_s(ctx, a, gout);
     return c ? launch_sweep_m_nv2_c(ctx, a, gout) : launch_sweep_m_nv2_s(ctx, a, gout);
   }
   if (exact || a.form == GF_EXACT) return nv == 1 ? launch_sweep_exact_nv1(ctx, a, gout) : launch_sweep_exact_nv2(ctx, a, gout);

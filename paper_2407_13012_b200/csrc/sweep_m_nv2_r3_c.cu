@@ -1,0 +1,9 @@
+// Merged-sweep instantiations: NV=2, R=3 family (16 warps, 8 amplitudes per vector per
+// thread), first-pass form C.
+#include "sweep_impl.cuh"
+
+namespace qsb {
+int launch_sweep_m_nv2_r3_c(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
+  return sweepk::launch_merged_f1<2, SM_MERGED, GF_FACT_C, SH_A3, SH_B3>(ctx, a, g);
+}
+}  // namespace qsb

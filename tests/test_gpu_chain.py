@@ -91,7 +91,7 @@ def test_chain_float_table(monkeypatch):
     assert rel_err(psi, want_psi) <= 1e-10
 
 
-@pytest.mark.parametrize("fam", ["5", "6"])
+@pytest.mark.parametrize("fam", ["5", "6", "r2m3"])
 @pytest.mark.parametrize("n,p", [(21, 2), (27, 2), (30, 2)])
 def test_chain_register_families(n, p, fam, monkeypatch):
     """single-vector sweeps with 32 amplitudes per thread (R=5: B windows need one
@@ -100,8 +100,11 @@ def test_chain_register_families(n, p, fam, monkeypatch):
     poly = random_instance(300 + n, n)
     params = params_wide(11 * n + p, p)
     ref = run(poly, params, monkeypatch, merge=True)
-    monkeypatch.setenv("QSB_SWEEP_R1M", fam)
-    monkeypatch.setenv("QSB_SWEEP_R1", fam)
+    if fam == "r2m3":  # merged bra/ket sweeps with 16 warps x 8 amplitudes per vector
+        monkeypatch.setenv("QSB_SWEEP_R2M", "3")
+    else:
+        monkeypatch.setenv("QSB_SWEEP_R1M", fam)
+        monkeypatch.setenv("QSB_SWEEP_R1", fam)
     got = run(poly, params, monkeypatch, merge=True)
     assert abs(got[0] - ref[0]) <= 1e-12 * max(1.0, abs(ref[0]))
     assert rel_err(got[1], ref[1]) <= 1e-12

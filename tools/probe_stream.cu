@@ -214,6 +214,163 @@ __global__ void __launch_bounds__(256, 1) k_btile(const __grid_constant__ CUtens
   }
 }
 
+// Generalised A-window probe: NV vectors (2: bra/ket with slots 2k%3 / (2k+1)%3 as in
+// the library), MERGED = two gate passes (phases 0,1,2 then 2,1,0), XSUM = bra/ket
+// contraction after each phase's gates.
+template <int NV, bool MERGED, int XSUM, int MID = 0>
+__global__ void __launch_bounds__(256, 1) k_probe(double2* __restrict__ v0g, double2* __restrict__ v1g, uint64_t ntiles,
+                                                   double gb, double* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  // MID: the diagonal between the passes as the library does it for a u8 table: index
+  // byte from a 4 KB tile in smem, (cos, sin) from a 41-entry LUT in smem, <bra|C|ket>
+  // accumulation, complex multiply of both vectors
+  uint8_t* cidx = smem + kRing * kSlot + 64;
+  double2* lut = (double2*)(cidx + kTile);
+  for (int i = threadIdx.x; i < kTile; i += 256) cidx[i] = (uint8_t)((i * 2654435761u) >> 26) % 41;
+  for (int i = threadIdx.x; i < 64; i += 256) lut[i] = make_double2(cos(0.1 * i), sin(0.1 * i));
+  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t bars = ring + kRing * kSlot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < kRing; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bars + 8 * s));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const uint64_t nseq = mine * NV;
+  auto issue = [&](uint64_t sq) {
+    if (tid != 0 || sq >= nseq) return;
+    const uint64_t k = sq / NV;
+    const int q = NV == 2 ? (int)((sq & 1) ^ 1) : 0;
+    const uint64_t t = blockIdx.x + k * gridDim.x;
+    const uint32_t slot = (uint32_t)(sq % kRing), bar = bars + 8 * slot;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kSlot) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     ring + slot * kSlot),
+                 "l"((q == 0 ? v0g : v1g) + (t << kT)), "r"(kSlot), "r"(bar)
+                 : "memory");
+  };
+  auto wait = [&](uint64_t sq) { mbar_wait(bars + 8 * (uint32_t)(sq % kRing), (uint32_t)((sq / kRing) & 1)); };
+  double acc = 0.0;
+  issue(0);
+  issue(1);
+  if (NV == 2) issue(2);
+  for (uint64_t k = 0; k < mine; ++k) {
+    const uint64_t t = blockIdx.x + k * gridDim.x;
+    uint32_t sk, sb = 0;
+    double2 v[NV][16];
+    const uint32_t lb0 = mbase(map_of(0), lane, warp);
+    if (NV == 1) {
+      issue(k + 2);
+      wait(k);
+      sk = ring + (uint32_t)(k % kRing) * kSlot;
+    } else {
+      sb = ring + (uint32_t)((2 * k) % kRing) * kSlot;
+      sk = ring + (uint32_t)((2 * k + 1) % kRing) * kSlot;
+      wait(2 * k);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[NV - 1][j] = lds(sb + (lb0 | (j << 8)) * 16u);
+      wait(2 * k + 1);
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[0][j] = lds(sk + (lb0 | (j << 8)) * 16u);
+    uint32_t cpk[4] = {0, 0, 0, 0};
+    if (MID == 2) {  // prefetch the mid-op index bytes now, packed 4 per register
+      const uint32_t lm = mbase(map_of(2), lane, warp);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) cpk[j >> 2] |= (uint32_t)cidx[lm | (j << map_of(2).reg)] << (8 * (j & 3));
+    }
+    auto exch = [&](int qi, int pi) {
+      const Map Q = map_of(qi), P = map_of(pi);
+      const uint32_t qb = mbase(Q, lane, warp), pb = mbase(P, lane, warp);
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < NV; ++q)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sts((q == 0 ? sk : sb) + swz(qb | (j << Q.reg)) * 16u, v[q][j]);
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < NV; ++q)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[q][j] = lds((q == 0 ? sk : sb) + swz(pb | (j << P.reg)) * 16u);
+    };
+    auto gates = [&]() {
+      double x[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = 0.0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (!(j & (1 << b))) {
+#pragma unroll
+            for (int q = 0; q < NV; ++q) bfly(v[q][j], v[q][j | (1 << b)], gb);
+          }
+      if (XSUM && NV == 2) {  // after the gates (X_j commutes with the layer)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (!(j & (1 << b))) {
+              const int k2 = j | (1 << b);
+              const int sl = XSUM == 1 ? 0 : XSUM == 2 ? (j & 3) : ((j & ((1 << b) - 1)) | ((j >> (b + 1)) << b));
+              x[sl] = fma(v[1][j].x, v[0][k2].y, x[sl]);
+              x[sl] = fma(-v[1][j].y, v[0][k2].x, x[sl]);
+              x[sl] = fma(v[1][k2].x, v[0][j].y, x[sl]);
+              x[sl] = fma(-v[1][k2].y, v[0][j].x, x[sl]);
+            }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc += x[i];
+      }
+    };
+    gates();
+    exch(0, 1);
+    gates();
+    exch(1, 2);
+    gates();
+    int last = 2;
+    if (MERGED && MID) {
+      const uint32_t lm = mbase(map_of(2), lane, warp);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t l = lm | (j << map_of(2).reg);
+        const int ci = MID == 2 ? (int)((cpk[j >> 2] >> (8 * (j & 3))) & 0xffu) : (int)cidx[l];
+        const double tv = -40.0 + (double)ci;
+        if (NV == 2) acc = fma(tv, v[1][j].x * v[0][j].y - v[1][j].y * v[0][j].x, acc);
+        const double2 f = lut[ci];
+#pragma unroll
+        for (int q = 0; q < NV; ++q)
+          v[q][j] = make_double2(fma(v[q][j].x, f.x, -v[q][j].y * f.y), fma(v[q][j].x, f.y, v[q][j].y * f.x));
+      }
+    }
+    if (MERGED) {
+      exch(2, 1);
+      gates();
+      exch(1, 0);
+      gates();
+      last = 0;
+    }
+    if (NV == 2) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      issue(2 * k + 3);
+      issue(2 * k + 4);
+    } else {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    const Map L = map_of(last);
+    const uint32_t lo = mbase(L, lane, warp);
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double2* d = (q == 0 ? v0g : v1g) + (t << kT);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) stg(d + (lo | (j << L.reg)), v[q][j]);
+    }
+    if (NV == 1) __syncthreads();
+  }
+  if (acc == 12345.0) out[0] = acc;
+}
+
 __global__ void k_ldg(const double2* __restrict__ src, double2* __restrict__ dst, uint64_t n, double scale) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     double2 v = __ldcs(src + i);
@@ -253,7 +410,7 @@ int main() {
   cudaMemset(a, 0x3f, N * 16);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const size_t smem = kRing * kSlot + 64;
+  const size_t smem = kRing * kSlot + 64 + kTile + 64 * 16;
   cudaFuncSetAttribute(k_stream<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_stream<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_stream<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -275,6 +432,51 @@ int main() {
                          "B L=3 glo=12", "B L=3 glo=21", "B L=3 glo=21, contiguous store", "B L=4 glo=18",
                          "B L=5 glo=18", "B L=2 glo=18", "B L=3 glo=21 promo none", "B L=3 glo=21 promo 128",
                          "B L=3 glo=21 2x grid (2 CTA/SM? no)"};
+  double* dout;
+  cudaMalloc(&dout, 64);
+  auto setp = [&](auto k) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); };
+  setp(k_probe<1, false, 0>);
+  setp(k_probe<1, true, 0>);
+  setp(k_probe<2, false, 0>);
+  setp(k_probe<2, false, 1>);
+  setp(k_probe<2, false, 2>);
+  setp(k_probe<2, false, 3>);
+  setp(k_probe<2, true, 0>);
+  setp(k_probe<2, true, 3>);
+  setp(k_probe<2, true, 3, 1>);
+  setp(k_probe<1, true, 0, 1>);
+  setp(k_probe<2, true, 3, 2>);
+  setp(k_probe<1, true, 0, 2>);
+  const char* pnames[] = {"probe A NV1 plain", "probe A NV1 merged", "probe A NV2 plain", "probe A NV2 plain+xsum(1 acc)",
+                          "probe A NV2 plain+xsum(4 acc)", "probe A NV2 plain+xsum(8 acc)", "probe A NV2 merged",
+                          "probe A NV2 merged+xsum(8 acc)", "probe A NV2 merged+xsum+mid", "probe A NV1 merged+mid", "probe A NV2 merged+xsum+mid(pf)", "probe A NV1 merged+mid(pf)"};
+  const double pbytes[] = {32.0, 32.0, 64.0, 64.0, 64.0, 64.0, 64.0, 64.0, 64.0, 32.0, 64.0, 32.0};
+  for (int m = 0; m < 12; ++m) {
+    float best = 1e9f;
+    for (int rep = 0; rep < 5; ++rep) {
+      cudaEventRecord(e0);
+      if (m == 0) k_probe<1, false, 0><<<sms, 256, smem>>>(a, b, ntiles, 0.3, dout);
+      if (m == 1) k_probe<1, true, 0><<<sms, 256, smem>>>(a, b, ntiles, 0.3, dout);
+      if (m == 2) k_probe<2, false, 0><<<sms, 256, smem>>>(a, b, ntiles, 0.3, dout);
+      if (m == 3) k_probe<2, false, 1><<<sms, 256, smem>>>(a, b, ntiles, 0.3, dout);
+      if (m == 4) k_probe<2, false, 2><<<sms, 256, smem>>>(a, b, ntiles, 0.3, dout);
+      if (m == 5) k_probe<2, false, 3><<<sms, 256, smem>>>(a, b, ntiles, 0.3, dout);
+      if (m == 6) k_probe<2, true, 0><<<sms, 256, smem>>>(a, b, ntiles, 0.3, dout);
+      if (m == 7) k_probe<2, true, 3><<<sms, 256, smem>>>(a, b, ntiles, 0.3, dout);
+      if (m == 8) k_probe<2, true, 3, 1><<<sms, 256, smem>>>(a, b, ntiles, 0.3, dout);
+      if (m == 9) k_probe<1, true, 0, 1><<<sms, 256, smem>>>(a, b, ntiles, 0.3, dout);
+      if (m == 10) k_probe<2, true, 3, 2><<<sms, 256, smem>>>(a, b, ntiles, 0.3, dout);
+      if (m == 11) k_probe<1, true, 0, 2><<<sms, 256, smem>>>(a, b, ntiles, 0.3, dout);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (ms < best) best = ms;
+    }
+    printf("%-34s: %.3f ms  %.1f GB/s  (%s)\n", pnames[m], best, pbytes[m] * N / (best * 1e-3) / 1e9,
+           cudaGetErrorString(cudaGetLastError()));
+  }
+  return 0;
   for (int mode = 0; mode < 13; ++mode) {
     float best = 1e9f;
     for (int rep = 0; rep < 5; ++rep) {
