@@ -50,6 +50,14 @@ std::vector<SweepShape> plan_range(int n, int lo, int hi) {
 
 std::vector<SweepShape> plan_sweeps(int n) { return plan_range(n, 0, n - 1); }
 
+// QSB_PAIR=1 launches single-vector B sweeps as lock-stepped 2-CTA clusters (256-byte
+// DRAM runs).  Off by default: +5% on plain single-vector B sweeps, but slower for
+// merged and bra/ket sweeps, whose per-tile times vary more (profiles/).
+bool pair_enabled() {
+  const char* e = getenv("QSB_PAIR");
+  return e && atoi(e) == 1;
+}
+
 // register-bit family of the fast sweeps: 4 by default; overrides QSB_SWEEP_R1 /
 // QSB_SWEEP_R2 (plain sweeps, 3..6 / 3..4) and QSB_SWEEP_R1M (merged single-vector
 // sweeps, 4..6; merged bra/ket sweeps are R=4 only).  6 = the R=5 shapes with two
@@ -348,6 +356,7 @@ struct Runner {
     const int gates = build_shape(sh, n, nv, exact, a, gbp, mode != SM_PLAIN ? pass2 : nullptr, gbp2, &gates2, mode);
     if (gates < 0) return invalid("internal: bad sweep layout");
     a.mode = mode;
+    a.want_pair = (pair_enabled() && nv == 1) ? 1 : 0;
     a.v0 = v0;
     a.v1 = v1;
     set_table(a, t);

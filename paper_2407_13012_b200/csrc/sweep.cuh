@@ -80,6 +80,8 @@ struct SweepArgs {
   int form2;
   int mode;
   int groups;             // warp groups per CTA (1, or 2 for the R=5 single-vector family "6")
+  int want_pair;          // host: B sweeps may run as 2-CTA clusters (QSB_PAIR=1, fused.cu)
+  int pair;               // set at launch: this launch is paired (cluster barrier per tile)
   double* partials;       // [kSlots][gridDim.x]
   uint64_t ntiles;
   uint32_t flags;

@@ -300,7 +300,14 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     issue(1);
     if constexpr (NV == 2 || GR == 2) issue(2);
   }
-  for (uint64_t k = grp; k < my_tiles; k += GR) {
+  // Paired launch (B windows): CTAs 2c, 2c+1 form a cluster and work on tiles that
+  // differ only in global bit 3 -- the two 128-byte halves of the same 256-byte runs.
+  // A cluster barrier per tile keeps them in step, so DRAM sees 256-byte requests
+  // (measured 4.6 -> 6.2 TB/s for the bare B-tile stream, profiles/r1e_probe_stream.txt).
+  // Both CTAs must pass the same number of barriers: iterate to the larger tile count.
+  const uint64_t iters = a.pair ? (a.ntiles + gridDim.x - 1) / gridDim.x : my_tiles;
+  for (uint64_t k = grp; k < iters; k += GR) {
+   if (k < my_tiles) {
     const uint64_t base = tile_base(a, blockIdx.x + k * gridDim.x);
     const uint8_t* cs = cring + (uint32_t)(k % kRing) * kCBytes;
     const uint32_t tb8 = (uint32_t)((blockIdx.x + k * gridDim.x) & 1u) << 3;  // cmode 2: tile's half of each row
@@ -566,6 +573,11 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
       gsync();  // the slot may be refilled from here on
       if constexpr (GR == 2) issue(k + 3);
     }
+   }  // k < my_tiles
+    if (a.pair) {
+      asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
   }
 
   // ------------------------------------------------------------ partial sums
@@ -616,7 +628,25 @@ struct SweepKernel {
   static int launch(qsb_ctx* ctx, SweepArgs& a, unsigned* gout) {
     unsigned g;
     QSB_TRY(grid(ctx, a.ntiles, &g));
-    k_sweep<SH, NV, FORM, KSIN, FULL, MODE, FORM2, GR, FM><<<g, threads, kSmemBytes, ctx->stream>>>(a);
+    // B windows run as 2-CTA clusters (see the kernel) when the grid allows it
+    a.pair = (!shape_is_a(SH) && GR == 1 && (g % 2) == 0 && a.want_pair) ? 1 : 0;
+    if (a.pair) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(g);
+      cfg.blockDim = dim3(threads);
+      cfg.dynamicSmemBytes = kSmemBytes;
+      cfg.stream = ctx->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      QSB_CUDA(cudaLaunchKernelEx(&cfg, k_sweep<SH, NV, FORM, KSIN, FULL, MODE, FORM2, GR, FM>, a));
+    } else {
+      k_sweep<SH, NV, FORM, KSIN, FULL, MODE, FORM2, GR, FM><<<g, threads, kSmemBytes, ctx->stream>>>(a);
+    }
     QSB_CHECK_LAUNCH(ctx, "sweep");
     if (gout) *gout = g;
     return QSB_OK;

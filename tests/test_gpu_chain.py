@@ -91,7 +91,7 @@ def test_chain_float_table(monkeypatch):
     assert rel_err(psi, want_psi) <= 1e-10
 
 
-@pytest.mark.parametrize("fam", ["5", "6", "r2m3"])
+@pytest.mark.parametrize("fam", ["5", "6", "r2m3", "pair"])
 @pytest.mark.parametrize("n,p", [(21, 2), (27, 2), (30, 2)])
 def test_chain_register_families(n, p, fam, monkeypatch):
     """single-vector sweeps with 32 amplitudes per thread (R=5: B windows need one
@@ -102,6 +102,8 @@ def test_chain_register_families(n, p, fam, monkeypatch):
     ref = run(poly, params, monkeypatch, merge=True)
     if fam == "r2m3":  # merged bra/ket sweeps with 16 warps x 8 amplitudes per vector
         monkeypatch.setenv("QSB_SWEEP_R2M", "3")
+    elif fam == "pair":  # single-vector B sweeps as lock-stepped 2-CTA clusters
+        monkeypatch.setenv("QSB_PAIR", "1")
     else:
         monkeypatch.setenv("QSB_SWEEP_R1M", fam)
         monkeypatch.setenv("QSB_SWEEP_R1", fam)

@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(256, 1) k_stream(const double2* __restrict__ s
 
 // B tile with L contiguous low bits (runs of 2^L amplitudes) and 12-L window bits at
 // glo; SC: store contiguous (tile order) instead of back to the strided positions
-template <int L, bool SC>
+template <int L, bool SC, int CL = 1>
 __global__ void __launch_bounds__(256, 1) k_btile(const __grid_constant__ CUtensorMap tm, double2* __restrict__ dst,
                                                   uint64_t ntiles, int glo, double scale) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -211,6 +211,10 @@ __global__ void __launch_bounds__(256, 1) k_btile(const __grid_constant__ CUtens
       else stg(dst + (base | (l & ((1u << L) - 1)) | ((uint64_t)(l >> L) << glo)), v[j]);
     }
     __syncthreads();
+    if (CL > 1) {  // keep the cluster's CTAs (adjacent 128 B runs) in lockstep
+      asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
   }
 }
 
@@ -431,7 +435,8 @@ int main() {
   const char* names[] = {"tma1d+stg", "tma1d+2exch+stg", "tma1d+tma-store", "ldg/stg", "A-window full sweep work",
                          "B L=3 glo=12", "B L=3 glo=21", "B L=3 glo=21, contiguous store", "B L=4 glo=18",
                          "B L=5 glo=18", "B L=2 glo=18", "B L=3 glo=21 promo none", "B L=3 glo=21 promo 128",
-                         "B L=3 glo=21 2x grid (2 CTA/SM? no)"};
+                         "B L=3 glo=21 2x grid (2 CTA/SM? no)", "B L=3 glo=21 cluster-2 lockstep",
+                         "B L=3 glo=21 cluster-4 lockstep", "B L=3 glo=12 cluster-2 lockstep"};
   double* dout;
   cudaMalloc(&dout, 64);
   auto setp = [&](auto k) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); };
@@ -476,8 +481,10 @@ int main() {
     printf("%-34s: %.3f ms  %.1f GB/s  (%s)\n", pnames[m], best, pbytes[m] * N / (best * 1e-3) / 1e9,
            cudaGetErrorString(cudaGetLastError()));
   }
-  return 0;
-  for (int mode = 0; mode < 13; ++mode) {
+  cudaFuncSetAttribute(k_btile<3, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_btile<3, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  for (int mode = 0; mode < 16; ++mode) {
+    if (mode == 12) continue;
     float best = 1e9f;
     for (int rep = 0; rep < 5; ++rep) {
       cudaEventRecord(e0);
@@ -494,6 +501,24 @@ int main() {
       if (mode == 10) k_btile<2, false><<<sms, 256, smem>>>(m2, b, ntiles, 18, 1.0);
       if (mode == 11) k_btile<3, false><<<sms, 256, smem>>>(mp0, b, ntiles, 21, 1.0);
       if (mode == 12) k_btile<3, false><<<sms, 256, smem>>>(mp1, b, ntiles, 21, 1.0);
+      if (mode == 13 || mode == 14 || mode == 15) {
+        const int cl = mode == 13 ? 2 : mode == 14 ? 4 : 2;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(sms);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cl;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        const CUtensorMap& mm = mode == 15 ? m12 : m21;
+        const int gl = mode == 15 ? 12 : 21;
+        if (cl == 2) cudaLaunchKernelEx(&cfg, k_btile<3, false, 2>, mm, b, ntiles, gl, 1.0);
+        else cudaLaunchKernelEx(&cfg, k_btile<3, false, 4>, mm, b, ntiles, gl, 1.0);
+      }
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
@@ -502,6 +527,57 @@ int main() {
     }
     cudaError_t err = cudaGetLastError();
     printf("mode %d %-34s: %.3f ms  %.1f GB/s  (%s)\n", mode, names[mode], best, 32.0 * N / (best * 1e-3) / 1e9, cudaGetErrorString(err));
+  }
+  // ---- B tiles (L=3) with clusters of CL CTAs kept in lockstep, for several window positions
+  cudaFuncSetAttribute(k_btile<3, false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_btile<3, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // reference output (no cluster) for a correctness check
+  double2* ref;
+  cudaMalloc(&ref, N * 16);
+  const int glos[] = {12, 16, 21};
+  for (int gi = 0; gi < 3; ++gi) {
+    const int gl = glos[gi];
+    const CUtensorMap mm = bmap(a, n, gl, 3);
+    k_btile<3, false, 1><<<sms, 256, smem>>>(mm, ref, ntiles, gl, 1.0);
+    cudaDeviceSynchronize();
+    for (int cl : {1, 2, 4, 8}) {
+      float best = 1e9f;
+      for (int rep = 0; rep < 5; ++rep) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(cl == 8 ? 144 : sms);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cl;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaMemset(b, 0, N * 16);
+        cudaEventRecord(e0);
+        if (cl == 1) cudaLaunchKernelEx(&cfg, k_btile<3, false, 1>, mm, b, ntiles, gl, 1.0);
+        if (cl == 2) cudaLaunchKernelEx(&cfg, k_btile<3, false, 2>, mm, b, ntiles, gl, 1.0);
+        if (cl == 4) cudaLaunchKernelEx(&cfg, k_btile<3, false, 4>, mm, b, ntiles, gl, 1.0);
+        if (cl == 8) cudaLaunchKernelEx(&cfg, k_btile<3, false, 8>, mm, b, ntiles, gl, 1.0);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+      }
+      // compare b with ref on a sample
+      static double2 hb[4096], hr[4096];
+      bool same = true;
+      const uint64_t offs[3] = {0ull, N / 3, N - 4096};
+      for (uint64_t off : offs) {
+        cudaMemcpy(hb, b + off, sizeof(hb), cudaMemcpyDeviceToHost);
+        cudaMemcpy(hr, ref + off, sizeof(hr), cudaMemcpyDeviceToHost);
+        for (int q = 0; q < 4096; ++q) same = same && hb[q].x == hr[q].x && hb[q].y == hr[q].y;
+      }
+      printf("B L=3 glo=%2d cluster %d: %.3f ms  %.1f GB/s  same=%d (%s)\n", gl, cl, best, 32.0 * N / (best * 1e-3) / 1e9,
+             (int)same, cudaGetErrorString(cudaGetLastError()));
+    }
   }
   return 0;
 }
