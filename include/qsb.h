@@ -170,6 +170,18 @@ int qsb_value_and_grad(qsb_ctx* ctx, qsb_table* t, double* ket, double* bra, int
 int qsb_sample(qsb_ctx* ctx, qsb_table* t, const double* amps, int n, uint64_t shots, uint64_t seed,
                int64_t* idx_out, double* cost_out, double* total_out);
 
+/* Sharded sampling (no reference counterpart: the reference samples one host array,
+ * backend.py:261-299; SURVEY.md §8(e) "Sampling across GPUs").  A shard builds the
+ * levels of its 2^n_local-amplitude subtree (kept in the context) and reports its
+ * root; the caller combines the shard roots with the reference's pairwise
+ * association, draws u = U(seed, s) * total, descends the levels above the shards and
+ * hands each shard the residual u of the shots that land in it. */
+int qsb_sample_tree(qsb_ctx* ctx, const double* amps, int n_local, double* root_out);
+/* Descend the tree built by qsb_sample_tree for `count` shots with residuals u[]
+ * (HOST array); local indices and (t != NULL) costs go to HOST arrays. */
+int qsb_sample_descend(qsb_ctx* ctx, qsb_table* t, const double* amps, int n_local, uint64_t count, const double* u,
+                       int64_t* idx_out, double* cost_out);
+
 #ifdef __cplusplus
 }
 #endif

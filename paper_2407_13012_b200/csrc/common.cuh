@@ -53,6 +53,10 @@ struct qsb_ctx {
   // kept: re-allocating ~0.5 GB per draw costs more than the draw itself
   void* d_sample = nullptr;
   uint64_t sample_bytes = 0;
+  void* d_shots = nullptr;  // per-shot uniforms / indices / costs
+  uint64_t shots_bytes = 0;
+  int tree_n = -1;              // the state whose tree d_sample holds (qsb_sample_tree)
+  const void* tree_amps = nullptr;
   // pinned host staging for small results
   double* h_small = nullptr;  // 4096 doubles
   // reusable device buffer for small uploads (LUTs, terms)
@@ -89,6 +93,7 @@ int prof_mark(qsb_ctx* ctx, cudaEvent_t* ev);
 int ensure_scratch(qsb_ctx* ctx, uint64_t bytes);
 int ensure_small(qsb_ctx* ctx, uint64_t bytes);
 int ensure_sample_scratch(qsb_ctx* ctx, uint64_t bytes);
+int ensure_shot_scratch(qsb_ctx* ctx, uint64_t bytes);
 // build (cos, sin) of (sign * gamma * v) for v = vmin + k, k < nvals, with host libm
 // (the same values Python's math.cos/sin and numba give) and upload to t->d_lut.
 int upload_phase_lut(qsb_table* t, double ang_scale, double2 extra_scale, bool exact);

@@ -56,6 +56,7 @@ int ensure_sample_scratch(qsb_ctx* ctx, uint64_t bytes) {
     ctx->d_sample = nullptr;
     ctx->sample_bytes = 0;
   }
+  ctx->tree_n = -1;
   cudaError_t e = cudaMalloc(&ctx->d_sample, bytes);
   if (e == cudaErrorMemoryAllocation) {
     cudaGetLastError();
@@ -63,6 +64,19 @@ int ensure_sample_scratch(qsb_ctx* ctx, uint64_t bytes) {
   }
   QSB_CUDA(e);
   ctx->sample_bytes = bytes;
+  return QSB_OK;
+}
+
+int ensure_shot_scratch(qsb_ctx* ctx, uint64_t bytes) {
+  if (bytes <= ctx->shots_bytes) return QSB_OK;
+  if (ctx->d_shots) {
+    QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    QSB_CUDA(cudaFree(ctx->d_shots));
+    ctx->d_shots = nullptr;
+    ctx->shots_bytes = 0;
+  }
+  QSB_CUDA(cudaMalloc(&ctx->d_shots, bytes));
+  ctx->shots_bytes = bytes;
   return QSB_OK;
 }
 
@@ -142,6 +156,7 @@ int qsb_ctx_destroy(qsb_ctx* ctx) {
   if (ctx->d_scratch) cudaFree(ctx->d_scratch);
   if (ctx->d_small) cudaFree(ctx->d_small);
   if (ctx->d_sample) cudaFree(ctx->d_sample);
+  if (ctx->d_shots) cudaFree(ctx->d_shots);
   if (ctx->h_small) cudaFreeHost(ctx->h_small);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);

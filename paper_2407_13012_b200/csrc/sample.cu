@@ -109,12 +109,20 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+// u_in == nullptr: u_s = U(seed, s) * root (the reference's draw); else u_s = u_in[s]
+// (a shard's residuals after the caller descended the levels above it).
 __global__ void k_descend(const double2* __restrict__ amps, Levels L, const double* __restrict__ table, uint64_t shots,
-                          uint64_t seed, double root, int64_t* __restrict__ idx_out, double* __restrict__ cost_out) {
+                          uint64_t seed, double root, const double* __restrict__ u_in, int64_t* __restrict__ idx_out,
+                          double* __restrict__ cost_out) {
   for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < shots; s += (uint64_t)gridDim.x * blockDim.x) {
-    // rng.uniform_block(seed, 0, shots)[s] * total  (rng.py:40-47, backend.py:291)
-    const uint64_t z = mix64(seed + (s + 1) * 0x9E3779B97F4A7C15ull);
-    double u = __dmul_rn(__dmul_rn((double)(z >> 11), 0x1.0p-53), root);
+    double u;
+    if (u_in) {
+      u = u_in[s];
+    } else {
+      // rng.uniform_block(seed, 0, shots)[s] * total  (rng.py:40-47, backend.py:291)
+      const uint64_t z = mix64(seed + (s + 1) * 0x9E3779B97F4A7C15ull);
+      u = __dmul_rn(__dmul_rn((double)(z >> 11), 0x1.0p-53), root);
+    }
     uint64_t idx = 0;  // node at level l+1
     for (int l = L.n - 1; l >= L.k0; --l) {
       const double left = L.base[L.off(l) + 2 * idx];
@@ -157,6 +165,52 @@ __global__ void k_descend(const double2* __restrict__ amps, Levels L, const doub
   }
 }
 
+// Build the stored levels of the n-qubit state's probability tree into the context's
+// sampler scratch; *root = its root (the total probability).
+int build_tree(qsb_ctx* ctx, const double2* a, int n, Levels* Lout, double* root) {
+  const uint64_t N = 1ull << n;
+  const int k0 = n < kK0 ? n : kK0;
+  Levels L{nullptr, N, n, k0};
+  QSB_TRY(ensure_sample_scratch(ctx, L.count() * sizeof(double)));
+  L.base = (double*)ctx->d_sample;
+  for (int l0 = 0; l0 < n; l0 += 11) {
+    const uint64_t M = N >> l0;
+    const uint64_t blocks = (M + kBIn - 1) / kBIn;
+    k_build<<<(unsigned)blocks, kBT, 0, ctx->stream>>>(a, L, l0);
+    QSB_CHECK_LAUNCH(ctx, "sample tree build");
+  }
+  QSB_CUDA(cudaMemcpyAsync(ctx->h_small, L.base + L.off(n), sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->d2h_bytes += sizeof(double);
+  *root = ctx->h_small[0];
+  *Lout = L;
+  return QSB_OK;
+}
+
+// Descend `shots` shots on the tree in L (uniforms from the seed, or u_host); indices
+// and costs copied to the host arrays.
+int descend(qsb_ctx* ctx, qsb_table* t, const double2* a, const Levels& L, uint64_t shots, uint64_t seed, double root,
+            const double* u_host, int64_t* idx_out, double* cost_out) {
+  QSB_TRY(ensure_shot_scratch(ctx, shots * (sizeof(int64_t) + sizeof(double) + (u_host ? sizeof(double) : 0))));
+  int64_t* d_idx = (int64_t*)ctx->d_shots;
+  double* d_cost = (double*)(d_idx + shots);
+  double* d_u = u_host ? d_cost + shots : nullptr;
+  if (u_host) {
+    QSB_CUDA(cudaMemcpyAsync(d_u, u_host, shots * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    ctx->h2d_bytes += shots * sizeof(double);
+  }
+  uint64_t blocks = (shots + 255) / 256;
+  if (blocks > (uint64_t)ctx->num_sms * 64) blocks = (uint64_t)ctx->num_sms * 64;
+  k_descend<<<(unsigned)blocks, 256, 0, ctx->stream>>>(a, L, t ? t->values : nullptr, shots, seed, root, d_u, d_idx,
+                                                        t ? d_cost : nullptr);
+  QSB_CHECK_LAUNCH(ctx, "sample descent");
+  QSB_CUDA(cudaMemcpyAsync(idx_out, d_idx, shots * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  if (t) QSB_CUDA(cudaMemcpyAsync(cost_out, d_cost, shots * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->d2h_bytes += shots * (sizeof(int64_t) + (t ? sizeof(double) : 0));
+  return QSB_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -168,50 +222,38 @@ int qsb_sample(qsb_ctx* ctx, qsb_table* t, const double* amps, int n, uint64_t s
   if (n < 1 || n > 62) return invalid("qsb_sample: n=%d out of range", n);
   if (t && n != t->n) return invalid("qsb_sample: state has n=%d, table n=%d", n, t->n);
   if (t && !cost_out) return invalid("qsb_sample: table given without a cost output");
-  const uint64_t N = 1ull << n;
   const double2* a = (const double2*)amps;
+  Levels L;
   double root;
-  const int k0 = n < kK0 ? n : kK0;
-  Levels L{nullptr, N, n, k0};
-  // scratch: levels k0..n, then the shot outputs (indices, costs)
-  const uint64_t lv_bytes = (L.count() * sizeof(double) + 255) & ~255ull;
-  QSB_TRY(ensure_sample_scratch(ctx, lv_bytes + shots * (sizeof(int64_t) + sizeof(double))));
-  double* levels = (double*)ctx->d_sample;
-  int64_t* d_idx = (int64_t*)((char*)ctx->d_sample + lv_bytes);
-  double* d_cost = t ? (double*)(d_idx + shots) : nullptr;
-  L.base = levels;
-  int rc = QSB_OK;
-  for (int l0 = 0; l0 < n; l0 += 11) {
-    const uint64_t M = N >> l0;
-    const uint64_t blocks = (M + kBIn - 1) / kBIn;
-    k_build<<<(unsigned)blocks, kBT, 0, ctx->stream>>>(a, L, l0);
-    ctx->launches++;
-  }
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) rc = cuda_fail(e, "sample tree build");
-  if (rc == QSB_OK) {
-    e = cudaMemcpyAsync(ctx->h_small, levels + L.off(n), sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-    if (e != cudaSuccess) rc = cuda_fail(e, "sample root");
-  }
-  if (rc == QSB_OK) {
-    root = ctx->h_small[0];
-    if (total_out) *total_out = root;
-    if (!(fabs(root - 1.0) <= 1e-9)) rc = invalid("state is not normalized: sum of probabilities = %.17g", root);
-  }
-  if (rc == QSB_OK) {
-    uint64_t blocks = (shots + 255) / 256;
-    if (blocks > (uint64_t)ctx->num_sms * 64) blocks = (uint64_t)ctx->num_sms * 64;
-    k_descend<<<(unsigned)blocks, 256, 0, ctx->stream>>>(a, L, t ? t->values : nullptr, shots, seed, root, d_idx, d_cost);
-    ctx->launches++;
-    e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaMemcpyAsync(idx_out, d_idx, shots * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream);
-    if (e == cudaSuccess && t) e = cudaMemcpyAsync(cost_out, d_cost, shots * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-    if (e != cudaSuccess) rc = cuda_fail(e, "sample descent");
-    ctx->d2h_bytes += shots * (sizeof(int64_t) + (t ? sizeof(double) : 0)) + sizeof(double);
-  }
-  return rc;
+  ctx->tree_n = -1;  // the scratch no longer holds a qsb_sample_tree tree
+  QSB_TRY(build_tree(ctx, a, n, &L, &root));
+  if (total_out) *total_out = root;
+  if (!(fabs(root - 1.0) <= 1e-9)) return invalid("state is not normalized: sum of probabilities = %.17g", root);
+  return descend(ctx, t, a, L, shots, seed, root, nullptr, idx_out, cost_out);
+}
+
+int qsb_sample_tree(qsb_ctx* ctx, const double* amps, int n_local, double* root_out) {
+  if (!ctx || !amps || !root_out) return invalid("qsb_sample_tree: null argument");
+  if (n_local < 1 || n_local > 62) return invalid("qsb_sample_tree: n=%d out of range", n_local);
+  Levels L;
+  QSB_TRY(build_tree(ctx, (const double2*)amps, n_local, &L, root_out));
+  ctx->tree_n = n_local;
+  ctx->tree_amps = amps;
+  return QSB_OK;
+}
+
+int qsb_sample_descend(qsb_ctx* ctx, qsb_table* t, const double* amps, int n_local, uint64_t count, const double* u,
+                       int64_t* idx_out, double* cost_out) {
+  if (!ctx || !amps || (count && (!u || !idx_out))) return invalid("qsb_sample_descend: null argument");
+  if (ctx->tree_n != n_local || ctx->tree_amps != amps)
+    return invalid("qsb_sample_descend: no tree for this state (call qsb_sample_tree first)");
+  if (t && n_local != t->n) return invalid("qsb_sample_descend: shard has n=%d, table n=%d", n_local, t->n);
+  if (t && count && !cost_out) return invalid("qsb_sample_descend: table given without a cost output");
+  if (count == 0) return QSB_OK;
+  const uint64_t N = 1ull << n_local;
+  const int k0 = n_local < kK0 ? n_local : kK0;
+  Levels L{(double*)ctx->d_sample, N, n_local, k0};
+  return descend(ctx, t, (const double2*)amps, L, count, 0, 0.0, u, idx_out, cost_out);
 }
 
 }  // extern "C"

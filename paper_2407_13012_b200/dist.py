@@ -29,7 +29,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import _lib, backend, circuit, costpoly
+from . import _lib, backend, circuit, costpoly, rng, sampling
 from ._lib import DeviceArray, call
 from .errors import ContractViolation
 from .kernels import b200
@@ -132,6 +132,14 @@ class VirtualExchanger:
             total = total + s
         return total
 
+    def gather(self, local: list[float]) -> list[float]:
+        """one value per rank, rank order (all ranks are local)"""
+        return list(local)
+
+    def owned_sum(self, *arrays: np.ndarray) -> tuple[np.ndarray, ...]:
+        """element-wise sum over ranks of arrays each rank filled only where it owns the entry"""
+        return arrays
+
     def swap(self, vecs: list[DeviceArray], scratch: list[DeviceArray]) -> None:
         G = self.G
         chunk = len(vecs[0]) // G
@@ -165,6 +173,24 @@ class TorchExchanger:
         for t in out:  # rank order: deterministic, identical on every rank
             total = total + t.cpu().numpy()
         return total
+
+    def gather(self, local: list[float]) -> list[float]:
+        import torch
+
+        mine = torch.tensor(local, dtype=torch.float64, device=f"cuda:{self.device}")
+        out = [torch.empty_like(mine) for _ in range(self.G)]
+        self.dist.all_gather(out, mine)
+        return [float(x) for t in out for x in t.cpu().tolist()]
+
+    def owned_sum(self, *arrays: np.ndarray) -> tuple[np.ndarray, ...]:
+        import torch
+
+        res = []
+        for a in arrays:  # exactly one rank contributes each entry: the sum is exact
+            t = torch.as_tensor(a, device=f"cuda:{self.device}")
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+            res.append(t.cpu().numpy())
+        return tuple(res)
 
     def swap(self, vecs: list[DeviceArray], scratch: list[DeviceArray]) -> None:
         import torch
@@ -300,6 +326,61 @@ class ShardedHandle:
         for k, r in enumerate(self.ranks):
             out[global_index(self.layout, self.n, self.g, r, i)] = self.ket[k].to_host()
         return out
+
+    def draw(self, shots: int, seed: int) -> "sampling.SampleSet":
+        """Sample the sharded state (sampling.draw semantics: indices in draw order, the
+        reference's probability-tree association and splitmix64 uniforms, so the
+        indices equal those of the unsharded state's draw).
+
+        Shards build their subtrees on their GPUs (qsb_sample_tree); the G roots are
+        gathered and combined pairwise exactly like the reference's upper tree levels;
+        every rank draws u_s = U(seed, s) * total and descends those g levels (identical
+        arithmetic everywhere), then each shard descends its own shots on the device
+        (qsb_sample_descend) and the per-shot results are summed over ranks (one owner
+        per shot)."""
+        if shots < 1:
+            raise ContractViolation(f"shots must be >= 1, got {shots}")
+        if self.layout != 0:  # back to layout A: the rank bits are the top index bits
+            self.ex.swap(self.ket, self.scratch)
+            self.layout = 0
+        h = self.ctx.device.handle
+        local = []
+        for k in range(len(self.ranks)):
+            r = C.c_double()
+            call("qsb_sample_tree", h, self.ket[k].ptr, self.n_l, C.byref(r))
+            local.append(r.value)
+        levels = [np.asarray(self.ex.gather(local), dtype=np.float64)]  # level n_l .. n
+        while levels[-1].shape[0] > 1:
+            v = levels[-1]
+            levels.append(v[0::2] + v[1::2])
+        total = float(levels[-1][0])
+        if not abs(total - 1.0) <= 1e-9:
+            raise ContractViolation(f"state is not normalized: sum of probabilities = {total!r}")
+        u = rng.uniform_block(seed, 0, shots) * total
+        shard = np.zeros(shots, dtype=np.int64)
+        for j in range(self.g - 1, -1, -1):
+            left = levels[j][2 * shard]
+            right = u >= left
+            u = np.where(right, u - left, u)
+            shard = 2 * shard + right
+        idx = np.zeros(shots, dtype=np.int64)
+        cost = np.zeros(shots, dtype=np.float64)
+        for k, r in enumerate(self.ranks):
+            sel = np.flatnonzero(shard == r)
+            if sel.size == 0:
+                continue
+            if len(self.ranks) > 1:  # virtual shards share one context: rebuild this shard's tree
+                r_ = C.c_double()
+                call("qsb_sample_tree", h, self.ket[k].ptr, self.n_l, C.byref(r_))
+            ui = np.ascontiguousarray(u[sel])
+            li = np.empty(sel.size, dtype=np.int64)
+            ci = np.empty(sel.size, dtype=np.float64)
+            call("qsb_sample_descend", h, self.tables[0][k].table.ptr, self.ket[k].ptr, self.n_l, int(sel.size),
+                 ui.ctypes.data, li.ctypes.data, ci.ctypes.data)
+            idx[sel] = li | (int(r) << self.n_l)
+            cost[sel] = ci
+        idx, cost = self.ex.owned_sum(idx, cost)
+        return sampling.SampleSet(shots=shots, seed=seed, indices=idx, costs=cost)
 
     def simulate(self, params: circuit.QaoaParams, exact: bool = False) -> None:
         steps = program(self.n, self.g, params.gammas, params.betas, False, False)

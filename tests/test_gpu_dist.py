@@ -66,3 +66,21 @@ def test_sharded_weighted_and_float_tables():
         assert abs(value - e) <= 1e-10 * max(1.0, abs(e))
         assert rel_err(np.concatenate([dg, db]), np.concatenate([wdg, wdb])) <= 1e-10
         sh.close()
+
+
+@pytest.mark.parametrize("n,g", [(14, 1), (15, 2), (16, 3)])
+def test_sharded_draw_matches_the_unsharded_tree(n, g):
+    """sharded sampling: the same indices and costs as the reference's draw on the
+    gathered state (same tree association, same uniforms)"""
+    poly = random_instance(40 + n, n)
+    params = random_params(n + 5, 2)
+    sh = dist.ShardedHandle(poly, g, dist.VirtualExchanger(g))
+    sh.simulate(params)
+    state = sh.gather_state()
+    table = oracle.precompute_table(poly.weights, poly.masks, n)
+    ss = sh.draw(20000, 11)
+    idx, cost = oracle.sample(state, table, 20000, 11)
+    assert np.array_equal(ss.indices, idx)
+    assert np.array_equal(ss.costs, cost)
+    assert sh.layout == 0
+    sh.close()

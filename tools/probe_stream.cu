@@ -375,6 +375,58 @@ __global__ void __launch_bounds__(256, 1) k_probe(double2* __restrict__ v0g, dou
   if (acc == 12345.0) out[0] = acc;
 }
 
+// B tile whose 9 window bits are two groups: glo..glo+4 and the top four bits n-4..n-1
+__global__ void __launch_bounds__(256, 1) k_bsplit(const __grid_constant__ CUtensorMap tm, double2* __restrict__ dst,
+                                                   uint64_t ntiles, int glo, int n, double scale) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t bars = ring + kRing * kSlot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < kRing; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bars + 8 * s));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int lowbits = glo - 3, midbits = n - 4 - (glo + 5);
+  auto issue = [&](uint64_t k) {
+    if (tid != 0 || k >= mine) return;
+    const uint64_t t = blockIdx.x + k * gridDim.x;
+    const uint32_t slot = (uint32_t)(k % kRing), bar = bars + 8 * slot;
+    const int c1 = (int)(t & ((1ull << lowbits) - 1)), c3 = (int)(t >> lowbits);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kSlot) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+        "%6}], [%7];" ::"r"(ring + slot * kSlot),
+        "l"(&tm), "r"(0), "r"(c1), "r"(0), "r"(c3), "r"(0), "r"(bar)
+        : "memory");
+  };
+  issue(0);
+  issue(1);
+  for (uint64_t k = 0; k < mine; ++k) {
+    const uint64_t t = blockIdx.x + k * gridDim.x;
+    issue(k + 2);
+    mbar_wait(bars + 8 * (uint32_t)(k % kRing), (uint32_t)((k / kRing) & 1));
+    const uint32_t slot = ring + (uint32_t)(k % kRing) * kSlot;
+    const uint32_t lb = (uint32_t)lane | ((uint32_t)warp << 5);
+    double2 v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = lds(slot + (lb | (j << 8)) * 16u);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = make_double2(v[j].x * scale, v[j].y * scale);
+    const uint64_t base = ((t & ((1ull << lowbits) - 1)) << 3) | ((t >> lowbits) << (glo + 5));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t l = lb | (j << 8);
+      const uint64_t gidx = base | (l & 7) | ((uint64_t)((l >> 3) & 31) << glo) | ((uint64_t)(l >> 8) << (n - 4));
+      stg(dst + gidx, v[j]);
+    }
+    __syncthreads();
+  }
+  (void)midbits;
+}
+
 __global__ void k_ldg(const double2* __restrict__ src, double2* __restrict__ dst, uint64_t n, double scale) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     double2 v = __ldcs(src + i);
@@ -400,6 +452,24 @@ static CUtensorMap bmap(const double2* base, int n, int glo, int L,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r) printf("encode failed %d (L=%d glo=%d)\n", (int)r, L, glo);
+  return m;
+}
+
+static CUtensorMap bmap_split(const double2* base, int n, int glo) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+  CUtensorMap m;
+  // {bits 0-2 (16 doubles), tile-low glo-3 bits, 5 window bits, tile-mid bits, 4 top window bits}
+  const int mid = n - 4 - (glo + 5);
+  const cuuint64_t dims[5] = {16, 1ull << (glo - 3), 32, 1ull << mid, 16};
+  const cuuint64_t strides[4] = {128, (1ull << glo) * 16, (1ull << (glo + 5)) * 16, (1ull << (n - 4)) * 16};
+  const cuuint32_t box[5] = {16, 1, 32, 1, 16};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = ((EncodeFn)p)(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)base, dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r) printf("split encode failed %d\n", (int)r);
   return m;
 }
 
@@ -577,6 +647,29 @@ int main() {
       }
       printf("B L=3 glo=%2d cluster %d: %.3f ms  %.1f GB/s  same=%d (%s)\n", gl, cl, best, 32.0 * N / (best * 1e-3) / 1e9,
              (int)same, cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  // ---- TLB test at n=29: contiguous top window (bits 20..28: 512 distinct 2 MB pages per tile)
+  // vs a split window (bits 12..16 + 25..28: 16 pages per tile), same bytes
+  {
+    const int n2 = 29;
+    const uint64_t N2 = 1ull << n2, nt2 = N2 >> kT;
+    cudaFuncSetAttribute(k_bsplit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const CUtensorMap mc = bmap(a, n2, 20, 3), ms = bmap_split(a, n2, 12);
+    for (int v = 0; v < 2; ++v) {
+      float best = 1e9f;
+      for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(e0);
+        if (v == 0) k_btile<3, false><<<sms, 256, smem>>>(mc, b, nt2, 20, 1.0);
+        else k_bsplit<<<sms, 256, smem>>>(ms, b, nt2, 12, n2, 1.0);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms_;
+        cudaEventElapsedTime(&ms_, e0, e1);
+        if (ms_ < best) best = ms_;
+      }
+      printf("n=29 B L=3 %s: %.3f ms  %.1f GB/s (%s)\n", v == 0 ? "window 20..28 (512 pages/tile)" : "window 12..16+25..28 (16 pages)",
+             best, 32.0 * N2 / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
     }
   }
   return 0;
