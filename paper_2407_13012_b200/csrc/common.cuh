@@ -97,6 +97,9 @@ int ensure_shot_scratch(qsb_ctx* ctx, uint64_t bytes);
 // build (cos, sin) of (sign * gamma * v) for v = vmin + k, k < nvals, with host libm
 // (the same values Python's math.cos/sin and numba give) and upload to t->d_lut.
 int upload_phase_lut(qsb_table* t, double ang_scale, double2 extra_scale, bool exact);
+// per-call phase LUTs for compact tables: LUT k = t->d_lut + k * nvals holds (cos, sin)
+// of ang_scales[k] * v (times extras[k] unless exact), v = vmin + index (fused.cu)
+int prepare_luts(qsb_table* t, const std::vector<double>& ang_scales, const std::vector<double2>& extras, bool exact);
 }  // namespace qsb
 
 // ------------------------------------------------------------ device helpers

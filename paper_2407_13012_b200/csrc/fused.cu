@@ -21,10 +21,53 @@ int expectation_exact(qsb_ctx* ctx, const double* table, const double2* amps, ui
 int diag_inner_exact(qsb_ctx* ctx, const double2* a, const double* table, const double2* b, uint64_t len,
                      double* out2);
 int xsum_exact(qsb_ctx* ctx, const double2* a, const double2* b, uint64_t len, int nq, double* out2);
+// small.cu: the whole circuit in one CTA for n <= 11
+int small_run(qsb_ctx* ctx, qsb_table* t, double2* ket, int p, const double* gammas, const double* betas, int mode,
+              double* value, double* dg, double* db);
 }  // namespace qsb
 
 extern "C" int qsb_table_phase(qsb_ctx* ctx, qsb_table* t, double* amps, double gamma);
 extern "C" int qsb_diag_scale(qsb_ctx* ctx, double* amps, const double* table, uint64_t len);
+
+namespace qsb {
+// per-call LUT staging: k-th LUT = t->d_lut + k * nvals
+int prepare_luts(qsb_table* t, const std::vector<double>& ang_scales, const std::vector<double2>& extras, bool exact) {
+  if (t->kind == 0 || ang_scales.empty()) return QSB_OK;
+  qsb_ctx* ctx = t->ctx;
+  const size_t need = ang_scales.size() * (size_t)t->nvals;
+  // t->d_lut holds nvals entries from finish_table; grow to `need`
+  static_assert(sizeof(double2) == 16, "");
+  size_t cap = t->h_lutbuf.size() / 2;
+  if (cap < need) {
+    QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (t->d_lut) cudaFree(t->d_lut);
+    t->d_lut = nullptr;
+    QSB_CUDA(cudaMalloc(&t->d_lut, need * sizeof(double2)));
+    t->h_lutbuf.assign(2 * need, 0.0);
+  }
+  double* h = t->h_lutbuf.data();
+  for (size_t L = 0; L < ang_scales.size(); ++L) {
+    for (int k = 0; k < t->nvals; ++k) {
+      const double v = t->vmin + (double)k;
+      const double ang = ang_scales[L] * v;
+      double c = cos(ang), s = sin(ang);
+      if (!exact) {
+        const double2 e = extras[L];
+        const double c2 = c * e.x - s * e.y, s2 = c * e.y + s * e.x;
+        c = c2;
+        s = s2;
+      }
+      h[2 * (L * t->nvals + k)] = c;
+      h[2 * (L * t->nvals + k) + 1] = s;
+    }
+  }
+  QSB_CUDA(cudaStreamSynchronize(ctx->stream));  // previous users of d_lut are done
+  QSB_CUDA(cudaMemcpyAsync(t->d_lut, h, need * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h2d_bytes += need * sizeof(double2);
+  return QSB_OK;
+}
+
+}  // namespace qsb
 
 namespace {
 
@@ -222,43 +265,6 @@ double ipow(double x, int k) {
   double r = 1.0;
   for (int i = 0; i < k; ++i) r *= x;
   return r;
-}
-
-// per-call LUT staging: k-th LUT = t->d_lut + k * nvals
-int prepare_luts(qsb_table* t, const std::vector<double>& ang_scales, const std::vector<double2>& extras, bool exact) {
-  if (t->kind == 0 || ang_scales.empty()) return QSB_OK;
-  qsb_ctx* ctx = t->ctx;
-  const size_t need = ang_scales.size() * (size_t)t->nvals;
-  // t->d_lut holds nvals entries from finish_table; grow to `need`
-  static_assert(sizeof(double2) == 16, "");
-  size_t cap = t->h_lutbuf.size() / 2;
-  if (cap < need) {
-    QSB_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (t->d_lut) cudaFree(t->d_lut);
-    t->d_lut = nullptr;
-    QSB_CUDA(cudaMalloc(&t->d_lut, need * sizeof(double2)));
-    t->h_lutbuf.assign(2 * need, 0.0);
-  }
-  double* h = t->h_lutbuf.data();
-  for (size_t L = 0; L < ang_scales.size(); ++L) {
-    for (int k = 0; k < t->nvals; ++k) {
-      const double v = t->vmin + (double)k;
-      const double ang = ang_scales[L] * v;
-      double c = cos(ang), s = sin(ang);
-      if (!exact) {
-        const double2 e = extras[L];
-        const double c2 = c * e.x - s * e.y, s2 = c * e.y + s * e.x;
-        c = c2;
-        s = s2;
-      }
-      h[2 * (L * t->nvals + k)] = c;
-      h[2 * (L * t->nvals + k) + 1] = s;
-    }
-  }
-  QSB_CUDA(cudaStreamSynchronize(ctx->stream));  // previous users of d_lut are done
-  QSB_CUDA(cudaMemcpyAsync(t->d_lut, h, need * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
-  ctx->h2d_bytes += need * sizeof(double2);
-  return QSB_OK;
 }
 
 void set_table(SweepArgs& a, qsb_table* t) {
@@ -719,6 +725,8 @@ int qsb_simulate_expect(qsb_ctx* ctx, qsb_table* t, double* amps, int p, const d
   const bool exact = flags & QSB_EXACT;
   const int n = t->n;
   double2* a = (double2*)amps;
+  if (n < kSweepT && p > 0 && (flags & QSB_FROM_PLUS) && p <= 1000)
+    return small_run(ctx, t, a, p, gammas, betas, expect_out ? 1 : 0, expect_out, nullptr, nullptr);
   if (n < kSweepT || p == 0) {
     if (p == 0 && (flags & QSB_FROM_PLUS)) QSB_TRY(launch_fill_plus(ctx, a, t->len));
     else QSB_TRY(simulate_perop(ctx, t, a, p, gammas, betas, flags));
@@ -796,6 +804,8 @@ int qsb_value_and_grad(qsb_ctx* ctx, qsb_table* t, double* ket_, double* bra_, i
   const int n = t->n;
   double2* ket = (double2*)ket_;
   double2* bra = (double2*)bra_;
+  if (n < kSweepT && p <= 1000)
+    return small_run(ctx, t, ket, p, gammas, betas, skip_forward ? 3 : 2, value, d_gammas, d_betas);
   if (exact || n < kSweepT)
     return value_and_grad_perop(ctx, t, ket, bra, p, gammas, betas, flags, skip_forward, value, d_gammas, d_betas);
 

@@ -1,0 +1,248 @@
+// Whole-circuit kernel for small registers (n <= 11, N <= 2048 amplitudes).
+//
+// Below one 4096-amplitude tile the sweep machinery does not apply and the per-op
+// path is launch-bound (~1.5-2.6 ms per value_and_grad, one launch per qubit gate and a
+// host round trip per reduction).  Here ONE CTA keeps the ket, the bra and the cost
+// table in shared memory and runs the whole simulate / <C> / adjoint walk in a single
+// launch with the reference's arithmetic: host-computed Rx (c, s) and phase LUTs,
+// FMA-free products (numba_impl.py:47-72), qubits in ascending order
+// (backend.py:200-207) and neighbour-pair trees over the (zero-padded) 2048-element
+// block (numba_impl.py:89-126), xsum per qubit in ascending order
+// (numba_impl.py:200-226) -- bit-identical to the numba kernel set for integral tables.
+#include <math.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+using namespace qsb;
+using namespace qsbd;
+
+namespace {
+
+constexpr int kST = 256;            // threads
+constexpr int kSMax = 2048;         // amplitudes (n <= 11)
+constexpr int kSPer = kSMax / kST;  // reduction elements per thread (8 consecutive)
+
+struct SmallArgs {
+  double2* ket;          // global statevector (in: mode 3; out: the walked ket)
+  const double* table;   // f64 table T
+  const void* cidx;      // compact index (kind 1: u8, 2: u16) -> LUT entry
+  const double2* lut;    // kind 1/2: [2p][nvals] phase factors (forward layers, then inverse)
+  const double* rxcs;    // [2p][2] (c, s): forward Rx(-2 beta_i), then inverse Rx(+2 beta_i)
+  const double* ang;     // kind 0: [2p] angle scales (forward -gamma_i, inverse +gamma_i)
+  double* out;           // [0] <C>, [1..p] d_gamma, [p+1..2p] d_beta
+  double plus_amp;
+  int n, p, kind, nvals;
+  int mode;              // 0 simulate, 1 simulate + <C>, 2 value_and_grad, 3 gradient of the given ket
+  int want_value;
+};
+
+// Neighbour-pair tree over 2048 elements, thread t holding elements 8t..8t+7:
+// 3 register levels, 5 xor-shuffle levels, 3 levels over the 8 warp sums.
+__device__ double block_tree(double v[kSPer], double* wsum) {
+#pragma unroll
+  for (int w = kSPer / 2; w >= 1; w >>= 1)
+#pragma unroll
+    for (int e = 0; e < w; ++e) v[e] = __dadd_rn(v[2 * e], v[2 * e + 1]);
+  double x = v[0];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, 1 << k));
+  __syncthreads();  // wsum reuse
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = x;
+  __syncthreads();
+  double w8[kST / 32];
+#pragma unroll
+  for (int e = 0; e < kST / 32; ++e) w8[e] = wsum[e];
+#pragma unroll
+  for (int w = kST / 64; w >= 1; w >>= 1)
+#pragma unroll
+    for (int e = 0; e < w; ++e) w8[e] = __dadd_rn(w8[2 * e], w8[2 * e + 1]);
+  return w8[0];  // every thread holds the root
+}
+
+__global__ void __launch_bounds__(kST, 1) k_small(const SmallArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  double2* ket = (double2*)smem_raw;
+  double2* bra = ket + kSMax;
+  double* T = (double*)(bra + kSMax);
+  double* wsum = T + kSMax;  // 8 warp partials (x2 for re / im)
+  const int n = a.n, p = a.p, N = 1 << n, tid = threadIdx.x;
+
+  for (int i = tid; i < N; i += kST) T[i] = a.table[i];
+  if (a.mode == 3) {
+    for (int i = tid; i < N; i += kST) ket[i] = a.ket[i];
+  } else {
+    for (int i = tid; i < N; i += kST) ket[i] = make_double2(a.plus_amp, 0.0);
+  }
+  __syncthreads();
+
+  // ψ_i *= (cos(ang), sin(ang)), ang = scale * T_i (numba_impl.py:47-51)
+  auto phase = [&](double2* v, int layer) {
+    for (int i = tid; i < N; i += kST) {
+      double2 f;
+      if (a.kind == 1) f = a.lut[(size_t)layer * a.nvals + ((const uint8_t*)a.cidx)[i]];
+      else if (a.kind == 2) f = a.lut[(size_t)layer * a.nvals + ((const uint16_t*)a.cidx)[i]];
+      else {
+        double s, c;
+        sincos(__dmul_rn(a.ang[layer], T[i]), &s, &c);
+        f = make_double2(c, s);
+      }
+      v[i] = cmul_exact(v[i], f);
+    }
+    __syncthreads();
+  };
+  // Rx on qubits 0..n-1 ascending (numba_impl.py:60-72, backend.py:200-207)
+  auto rx_layer = [&](double2* v, int layer) {
+    const double c = a.rxcs[2 * layer], s = a.rxcs[2 * layer + 1];
+    for (int j = 0; j < n; ++j) {
+      const int low = (1 << j) - 1, bit = 1 << j;
+      for (int k = tid; k < (N >> 1); k += kST) {
+        const int i0 = ((k & ~low) << 1) | (k & low), i1 = i0 | bit;
+        const double2 t = v[i0], u = v[i1];
+        v[i0] = make_double2(__dadd_rn(__dmul_rn(c, t.x), __dmul_rn(s, u.y)), __dadd_rn(__dmul_rn(c, t.y), -__dmul_rn(s, u.x)));
+        v[i1] = make_double2(__dadd_rn(__dmul_rn(s, t.y), __dmul_rn(c, u.x)), __dadd_rn(__dmul_rn(c, u.y), -__dmul_rn(s, t.x)));
+      }
+      __syncthreads();
+    }
+  };
+
+  if (a.mode != 3) {
+    for (int i = 0; i < p; ++i) {
+      phase(ket, i);
+      rx_layer(ket, i);
+    }
+  }
+  if (a.want_value) {  // T_i * (re^2 + im^2), tree (numba_impl.py:75-79, 114-126)
+    double v[kSPer];
+#pragma unroll
+    for (int e = 0; e < kSPer; ++e) {
+      const int i = tid * kSPer + e;
+      v[e] = i < N ? __dmul_rn(T[i], norm2_exact(ket[i])) : 0.0;
+    }
+    const double r = block_tree(v, wsum);
+    if (tid == 0) a.out[0] = r;
+  }
+  if (a.mode >= 2) {
+    for (int i = tid; i < N; i += kST) bra[i] = make_double2(__dmul_rn(ket[i].x, T[i]), __dmul_rn(ket[i].y, T[i]));
+    __syncthreads();
+    for (int L = p - 1; L >= 0; --L) {
+      // xsum (numba_impl.py:200-226): per qubit a tree of conj(bra_i) ket_{i^bit}, += in ascending j
+      double xre = 0.0, xim = 0.0;
+      for (int j = 0; j < n; ++j) {
+        double vr[kSPer], vi[kSPer];
+#pragma unroll
+        for (int e = 0; e < kSPer; ++e) {
+          const int i = tid * kSPer + e;
+          if (i < N) {
+            const double2 pa = bra[i], q = ket[i ^ (1 << j)];
+            vr[e] = re_conj_mul_exact(pa, q);
+            vi[e] = im_conj_mul_exact(pa, q);
+          } else {
+            vr[e] = vi[e] = 0.0;
+          }
+        }
+        xre = __dadd_rn(xre, block_tree(vr, wsum));
+        xim = __dadd_rn(xim, block_tree(vi, wsum + kST / 32));
+      }
+      if (tid == 0) a.out[1 + p + L] = -2.0 * xim;
+      rx_layer(bra, p + L);
+      rx_layer(ket, p + L);
+      // <bra|C|ket> (numba_impl.py:173-197): products, then * T
+      double vr[kSPer], vi[kSPer];
+#pragma unroll
+      for (int e = 0; e < kSPer; ++e) {
+        const int i = tid * kSPer + e;
+        if (i < N) {
+          const double2 pa = bra[i], q = ket[i];
+          vr[e] = __dmul_rn(re_conj_mul_exact(pa, q), T[i]);
+          vi[e] = __dmul_rn(im_conj_mul_exact(pa, q), T[i]);
+        } else {
+          vr[e] = vi[e] = 0.0;
+        }
+      }
+      block_tree(vr, wsum);
+      const double di = block_tree(vi, wsum + kST / 32);
+      if (tid == 0) a.out[1 + L] = 2.0 * di;
+      phase(bra, p + L);
+      phase(ket, p + L);
+    }
+  }
+  for (int i = tid; i < N; i += kST) a.ket[i] = ket[i];
+}
+
+}  // namespace
+
+namespace qsb {
+
+// Host side: LUTs / angles / Rx coefficients for 2p layers (forward, then inverse),
+// one launch, one copy back.  mode: 0 simulate, 1 simulate + <C>, 2 value_and_grad,
+// 3 gradient of the ket as given.
+int small_run(qsb_ctx* ctx, qsb_table* t, double2* ket, int p, const double* gammas, const double* betas, int mode,
+              double* value, double* dg, double* db) {
+  const int n = t->n;
+  if (n > 11) return invalid("internal: small_run needs n <= 11");
+  const int L = 2 * (p > 0 ? p : 1);
+  std::vector<double> host(4 * L + 1 + 2 * p + 1, 0.0);
+  double* rxcs = host.data();          // [L][2]
+  double* ang = rxcs + 2 * L;          // [L]
+  for (int i = 0; i < p; ++i) {
+    const double tf = -2.0 * betas[i], ti = 2.0 * betas[i];  // circuit.py:103, adjoint.py:63-64
+    rxcs[2 * i] = cos(tf / 2.0);
+    rxcs[2 * i + 1] = sin(tf / 2.0);
+    rxcs[2 * (p + i)] = cos(ti / 2.0);
+    rxcs[2 * (p + i) + 1] = sin(ti / 2.0);
+    ang[i] = -gammas[i];      // forward phase exp(-i g C)
+    ang[p + i] = gammas[i];   // inverse phase (adjoint.py:67-68 phase(-gamma))
+  }
+  if (t->kind != 0) {
+    std::vector<double> sc(ang, ang + 2 * p);
+    std::vector<double2> ex(2 * p, make_double2(1.0, 0.0));
+    if (p > 0) QSB_TRY(prepare_luts(t, sc, ex, true));
+  }
+  const size_t in_bytes = (size_t)(3 * L) * sizeof(double);
+  const size_t out_doubles = 1 + 2 * (size_t)p;
+  QSB_TRY(ensure_small(ctx, in_bytes + out_doubles * sizeof(double) + 64));
+  double* d_in = (double*)ctx->d_small;
+  double* d_out = d_in + 3 * L;
+  QSB_CUDA(cudaMemcpyAsync(d_in, host.data(), in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h2d_bytes += in_bytes;
+  SmallArgs a;
+  a.ket = ket;
+  a.table = t->values;
+  a.cidx = t->cidx;
+  a.lut = t->d_lut;
+  a.rxcs = d_in;
+  a.ang = d_in + 2 * L;
+  a.out = d_out;
+  a.plus_amp = 1.0 / sqrt((double)(1ull << n));  // numba_impl.py:42
+  a.n = n;
+  a.p = p;
+  a.kind = t->kind;
+  a.nvals = t->nvals;
+  a.mode = mode;
+  a.want_value = value != nullptr;
+  const size_t smem = (size_t)kSMax * (16 + 16 + 8) + 2 * (kST / 32) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    QSB_CUDA(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  k_small<<<1, kST, smem, ctx->stream>>>(a);
+  QSB_CHECK_LAUNCH(ctx, "small-register circuit");
+  if (value || mode >= 2) {
+    double* h = ctx->h_small;
+    QSB_CUDA(cudaMemcpyAsync(h, d_out, out_doubles * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->d2h_bytes += out_doubles * sizeof(double);
+    if (value) *value = h[0];
+    if (mode >= 2)
+      for (int i = 0; i < p; ++i) {
+        dg[i] = h[1 + i];
+        db[i] = h[1 + p + i];
+      }
+  }
+  return QSB_OK;
+}
+
+}  // namespace qsb

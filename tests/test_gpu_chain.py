@@ -123,3 +123,25 @@ def test_gradient_without_value(n, p, monkeypatch):
     g2 = qs.gradient(h, params)
     h.close()
     assert rel_err(flat(g2), flat(g)) <= 1e-13
+
+
+@pytest.mark.parametrize("n,p", [(3, 1), (6, 3), (9, 2), (11, 4)])
+def test_small_register_kernel_is_bit_exact(n, p, monkeypatch):
+    """n <= 11: the whole circuit runs in one CTA with the reference's arithmetic
+    (small.cu) -- <C>, gradient and final state equal the numba-order oracle bit for
+    bit on integral tables, in fast and exact mode alike."""
+    poly = random_instance(900 + n, n)
+    params = params_wide(17 * n + p, p)
+    table = oracle.precompute_table(poly.weights, poly.masks, n)
+    want_psi = oracle.simulate(table, n, params.gammas, params.betas)
+    want_e = oracle.expectation(table, want_psi)
+    dg, db = oracle.gradient(table, want_psi.copy(), params.gammas, params.betas)
+    for exact in ("0", "1"):
+        monkeypatch.setenv("QAOA_B200_EXACT", exact)
+        h = qs.create_handle(poly, backend_name="b200")
+        v, g = qs.value_and_grad(h, params)
+        psi = np.asarray(qs.statevector(h, params))
+        h.close()
+        assert v == min(max(want_e, table.min()), table.max())
+        assert np.array_equal(np.array(g.d_gammas), dg) and np.array_equal(np.array(g.d_betas), db)
+        assert np.array_equal(psi, want_psi)
