@@ -93,12 +93,13 @@ std::vector<SweepShape> plan_range(int n, int lo, int hi) {
 
 std::vector<SweepShape> plan_sweeps(int n) { return plan_range(n, 0, n - 1); }
 
-// QSB_PAIR=1 launches single-vector B sweeps as lock-stepped 2-CTA clusters (256-byte
-// DRAM runs).  Off by default: +5% on plain single-vector B sweeps, but slower for
-// merged and bra/ket sweeps, whose per-tile times vary more (profiles/).
-bool pair_enabled() {
+// Plain single-vector B sweeps run as lock-stepped 2-CTA clusters (256-byte DRAM runs;
+// +5% on those sweeps).  Merged and bra/ket sweeps, whose per-tile times vary more,
+// measured slower paired and stay unpaired.  QSB_PAIR=0 disables, =2 pairs every
+// single-vector B sweep (A/B tests).
+int pair_mode() {
   const char* e = getenv("QSB_PAIR");
-  return e && atoi(e) == 1;
+  return e ? atoi(e) : 1;
 }
 
 // register-bit family of the fast sweeps: 4 by default; overrides QSB_SWEEP_R1 /
@@ -362,7 +363,10 @@ struct Runner {
     const int gates = build_shape(sh, n, nv, exact, a, gbp, mode != SM_PLAIN ? pass2 : nullptr, gbp2, &gates2, mode);
     if (gates < 0) return invalid("internal: bad sweep layout");
     a.mode = mode;
-    a.want_pair = (pair_enabled() && nv == 1) ? 1 : 0;
+    {
+      const int pm = pair_mode();
+      a.want_pair = (nv == 1 && ((pm == 1 && mode == SM_PLAIN) || pm == 2)) ? 1 : 0;
+    }
     a.v0 = v0;
     a.v1 = v1;
     set_table(a, t);

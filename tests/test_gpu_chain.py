@@ -103,7 +103,7 @@ def test_chain_register_families(n, p, fam, monkeypatch):
     if fam == "r2m3":  # merged bra/ket sweeps with 16 warps x 8 amplitudes per vector
         monkeypatch.setenv("QSB_SWEEP_R2M", "3")
     elif fam == "pair":  # single-vector B sweeps as lock-stepped 2-CTA clusters
-        monkeypatch.setenv("QSB_PAIR", "1")
+        monkeypatch.setenv("QSB_PAIR", "2")
     else:
         monkeypatch.setenv("QSB_SWEEP_R1M", fam)
         monkeypatch.setenv("QSB_SWEEP_R1", fam)
