@@ -293,6 +293,9 @@ def run_sharded(args, rank: int, world: int, dist) -> None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     n = args.n if args.n != N_QUBITS else N_QUBITS + g
     poly, params = workload(n, args.p, args.params)
+    # the qubit swap fused into the sweeps' stores over NVLink (CUDA IPC peer buffers);
+    # QSB_SHARD_P2P=0 falls back to an NCCL all-to-all after the A visit
+    os.environ.setdefault("QSB_SHARD_P2P", "1")
     ex = qdist.TorchExchanger(g, dist, local)
     t0 = time.perf_counter()
     sh = qdist.ShardedHandle(poly, g, ex, device=local)
@@ -336,8 +339,9 @@ def run_sharded(args, rank: int, world: int, dist) -> None:
             "data": "synthetic (reference graph generator, seed 1)",
             "config": {
                 "workload": f"sharded MaxCut regular graph n={n} (random_regular(n,{3 if n % 2 == 0 else 4},seed=1)) "
-                            f"over {world} GPUs (top {g} qubits global, NCCL all-to-all index-bit swaps), p={args.p}; "
-                            f"one step = expectation + full adjoint gradient",
+                            f"over {world} GPUs (top {g} qubits global; index-bit swap "
+                            f"{'fused into the sweep stores, NVLink P2P' if ex.fused else 'by NCCL all-to-all'}), "
+                            f"p={args.p}; one step = expectation + full adjoint gradient (window chain)",
                 "n": n, "p": args.p, "global_batch": 1, "parallelism": f"statevector sharded x{world}",
                 "value_definition": f"steps * 2^(n-30) / time: n=30-equivalent E+grad evaluations/s",
                 "l2": "no flush: 16 GiB per-GPU shard >> 126 MB L2",

@@ -50,6 +50,33 @@ extern "C" {
 #define QSB_SW_POST_DINNER 64u   /* nv=2: sums[0] += Im <bra|C|ket> after the gates */
 #define QSB_SW_NO_STORE 128u     /* results are not written back */
 #define QSB_SW_EXACT 65536u      /* FMA-free, ascending-order arithmetic */
+/* between the two gate passes of a merged / bridge visit (qsb_shard_visit) */
+#define QSB_SW_MID_PHASE 512u    /* multiply by exp(i * phase_scale * C) */
+#define QSB_SW_MID_DINNER 1024u  /* nv=2: sums[1] += Im <bra|C|ket> */
+#define QSB_SW_MID_EXPECT 2048u  /* bridge: sums[0] += <ket|C|ket> (then bra = C * ket) */
+#define QSB_SW_XSUM2 4096u       /* nv=2: sums[3] += xsum over the second pass's qubits */
+
+/* One window visit of the sharded window chain (paper_2407_13012_b200/dist.py).
+ * mode 0: one gate pass Rx(theta1) on positions [lo1, hi1] (+ pre / post ops);
+ * mode 1: merged -- pass 1, the mid ops, pass 2 Rx(theta2) on [lo2, hi2];
+ * mode 2: bridge -- pass 1 on the ket only, <C>, bra = C * ket, pass 2 on both.
+ * window: 0 = the A window (local bits 0..11), else a B window with its 9 bits at
+ * window..window+8.  swap_g > 0 fuses the qubit swap into the store: each output tile
+ * (whose top swap_g local bits are c) goes to out0[c] (out1[c] for the bra) at
+ * (local & (2^(n-swap_g)-1)) | (swap_rank << (n-swap_g)) -- peer shards' buffers over
+ * NVLink (P2P), or chunk c of a local staging buffer for an all-to-all. */
+typedef struct qsb_shard_visit {
+  int nv, mode, window;
+  int lo1, hi1;
+  double theta1;
+  int lo2, hi2;
+  double theta2;
+  unsigned flags;
+  double phase_scale;
+  int swap_g, swap_rank;
+  double* out0[8];
+  double* out1[8];
+} qsb_shard_visit;
 
 typedef struct qsb_ctx qsb_ctx;
 typedef struct qsb_table qsb_table;
@@ -83,6 +110,13 @@ int qsb_ctx_launches(qsb_ctx* ctx, uint64_t* out);
 /* ----------------------------------------------------- memory (backend.py allocation hooks) */
 int qsb_alloc(qsb_ctx* ctx, uint64_t bytes, void** dptr);            /* np.empty, backend.py:133,165 */
 int qsb_free(qsb_ctx* ctx, void* dptr);                              /* eager release (StateBuffer.free) */
+/* CUDA IPC of device buffers for the sharded walk's fused qubit swap (dist.py):
+ * export a 64-byte handle, open a peer process's buffer, close it; qsb_device_sync
+ * waits for every kernel of this process (peer stores included) to complete. */
+int qsb_ipc_handle(qsb_ctx* ctx, const void* dptr, void* handle64);
+int qsb_ipc_open(qsb_ctx* ctx, const void* handle64, void** dptr);
+int qsb_ipc_close(qsb_ctx* ctx, void* dptr);
+int qsb_device_sync(qsb_ctx* ctx);
 int qsb_h2d(qsb_ctx* ctx, void* dst, const void* src, uint64_t bytes);
 int qsb_d2h(qsb_ctx* ctx, void* dst, const void* src, uint64_t bytes);
 int qsb_d2d(qsb_ctx* ctx, void* dst, const void* src, uint64_t bytes); /* clone_state, backend.py:149 */
@@ -152,6 +186,11 @@ int qsb_rx_layer(qsb_ctx* ctx, double* amps, int n, double theta, unsigned flags
  * (see fused.cu).  Building block of the sharded walk. */
 int qsb_layer_sweeps(qsb_ctx* ctx, qsb_table* t, double* v0, double* v1, int nv, int n, int n_global, int lo,
                      int hi, double theta, unsigned flags, double phase_scale, double* sums);
+/* One visit of the sharded window chain (fast mode); sums[4] = {<C> or post / mid
+ * <bra|C|ket>... see qsb_shard_visit: slot 0 <C> / post dinner / bridge <C>, 1 pre or mid
+ * Im<bra|C|ket>, 2 xsum of pass 1, 3 xsum of pass 2}.  n = local qubits of the shard. */
+int qsb_shard_visit_run(qsb_ctx* ctx, qsb_table* t, double* v0, double* v1, int n, int n_global,
+                        const qsb_shard_visit* d, double* sums);
 /* <psi|C|psi> (circuit.expectation_of_state, circuit.py:106-113, without the clamp) */
 int qsb_expectation(qsb_ctx* ctx, qsb_table* t, const double* amps, unsigned flags, double* out);
 /* expectation + adjoint gradient (adjoint.py:37-77): one forward, one backward walk

@@ -84,6 +84,11 @@ _SIGS = {
     "qsb_value_and_grad": [_vp, _vp, _vp, _vp, _i32, _dp, _dp, C.c_uint, _i32, _dp, _dp, _dp],
     "qsb_sample": [_vp, _vp, _vp, _i32, _u64, _u64, _vp, _vp, _dp],
     "qsb_sample_tree": [_vp, _vp, _i32, _dp],
+    "qsb_shard_visit_run": [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _dp],
+    "qsb_ipc_handle": [_vp, _vp, _vp],
+    "qsb_ipc_open": [_vp, _vp, C.POINTER(_vp)],
+    "qsb_ipc_close": [_vp, _vp],
+    "qsb_device_sync": [_vp],
     "qsb_sample_descend": [_vp, _vp, _vp, _i32, _u64, _vp, _vp, _vp],
 }
 _RESTYPES = {"qsb_last_error": C.c_char_p, "qsb_abi_version": _i32}

@@ -270,6 +270,45 @@ int qsb_free(qsb_ctx* ctx, void* dptr) {
   return QSB_OK;
 }
 
+// CUDA IPC for the sharded walk's fused qubit swap: a shard's spare buffers are exported
+// (64-byte handles, exchanged by the host over torch.distributed) and opened by every
+// peer process, whose swap-store kernels then write straight into them over NVLink.
+int qsb_ipc_handle(qsb_ctx* ctx, const void* dptr, void* handle64) {
+  if (!ctx || !dptr || !handle64) return invalid("qsb_ipc_handle: null argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  QSB_CUDA(cudaSetDevice(ctx->device));
+  cudaIpcMemHandle_t h;
+  QSB_CUDA(cudaIpcGetMemHandle(&h, (void*)dptr));
+  memcpy(handle64, &h, 64);
+  return QSB_OK;
+}
+
+int qsb_ipc_open(qsb_ctx* ctx, const void* handle64, void** dptr) {
+  if (!ctx || !handle64 || !dptr) return invalid("qsb_ipc_open: null argument");
+  QSB_CUDA(cudaSetDevice(ctx->device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, 64);
+  QSB_CUDA(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return QSB_OK;
+}
+
+int qsb_ipc_close(qsb_ctx* ctx, void* dptr) {
+  if (!ctx) return invalid("qsb_ipc_close: null context");
+  if (!dptr) return QSB_OK;
+  QSB_CUDA(cudaSetDevice(ctx->device));
+  QSB_CUDA(cudaIpcCloseMemHandle(dptr));
+  return QSB_OK;
+}
+
+// device-wide completion: the stores of this process's kernels (including peer stores
+// over NVLink) are complete and visible once this returns
+int qsb_device_sync(qsb_ctx* ctx) {
+  if (!ctx) return invalid("qsb_device_sync: null context");
+  QSB_CUDA(cudaSetDevice(ctx->device));
+  QSB_CUDA(cudaDeviceSynchronize());
+  return QSB_OK;
+}
+
 int qsb_h2d(qsb_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
   if (!ctx) return invalid("null context");
   if (!bytes) return QSB_OK;

@@ -311,6 +311,7 @@ struct Runner {
   double* partials = nullptr;   // device, kSlots * maxgrid per sweep
   double plus_amp = 0.0;        // 0: 1/sqrt(2^n)
   unsigned maxgrid = 0;
+  const qsb_shard_visit* swap = nullptr;  // fused qubit-swap store (sharded walk)
 
   int init(int total_sweeps_upper) {
     shapes = plan_sweeps(n);
@@ -409,6 +410,15 @@ struct Runner {
       if (!exact && gates > 0) flags |= SF_POST_SCALE;
     }
     a.flags = flags;
+    if (swap && swap->swap_g) {
+      a.sw_g = swap->swap_g;
+      a.sw_rank = swap->swap_rank;
+      a.sw_nl = n;
+      for (int c = 0; c < (1 << swap->swap_g); ++c) {
+        a.sw_out[0][c] = (double2*)swap->out0[c];
+        a.sw_out[1][c] = (double2*)swap->out1[c];
+      }
+    }
     const int idx = nsweeps_launched++;
     a.partials = want_partials ? partials + (uint64_t)idx * kSlots * maxgrid : nullptr;
     unsigned grid = 0;
@@ -700,11 +710,55 @@ int qsb_layer_sweeps(qsb_ctx* ctx, qsb_table* t, double* v0, double* v1, int nv,
   return QSB_OK;
 }
 
+int qsb_shard_visit_run(qsb_ctx* ctx, qsb_table* t, double* v0, double* v1, int n, int n_global,
+                        const qsb_shard_visit* d, double* sums) {
+  if (!ctx || !t || !v0 || !d || !sums || (d->nv == 2 && !v1)) return invalid("qsb_shard_visit_run: null argument");
+  if (d->nv != 1 && d->nv != 2) return invalid("qsb_shard_visit_run: nv must be 1 or 2");
+  if (n < kSweepT || n > 62 || n != t->n) return invalid("qsb_shard_visit_run: n=%d (table n=%d, need >= 12)", n, t->n);
+  if (n_global < n || n_global > 62) return invalid("qsb_shard_visit_run: n_global=%d < n=%d", n_global, n);
+  if (d->mode < SM_PLAIN || d->mode > SM_BRIDGE || (d->mode == SM_BRIDGE && d->nv != 2))
+    return invalid("qsb_shard_visit_run: bad mode %d", d->mode);
+  SweepShape sh;
+  if (d->window == 0) {
+    sh = {true, d->lo1, d->hi1, 0};
+  } else {
+    if (d->window < 4 || d->window + 9 > n)
+      return invalid("qsb_shard_visit_run: B window at %d does not fit n=%d", d->window, n);
+    sh = {false, d->lo1, d->hi1, d->window};
+  }
+  const int wlo = sh.is_a ? 0 : sh.glo, whi = sh.is_a ? kSweepT - 1 : sh.glo + 8;
+  if (d->lo1 < wlo || d->hi1 > whi || d->lo1 > d->hi1) return invalid("qsb_shard_visit_run: pass 1 outside the window");
+  if (d->mode != SM_PLAIN && (d->lo2 < wlo || d->hi2 > whi || d->lo2 > d->hi2))
+    return invalid("qsb_shard_visit_run: pass 2 outside the window");
+  if (d->swap_g) {
+    if (d->swap_g < 1 || d->swap_g > 3 || n - d->swap_g < whi + 1)
+      return invalid("qsb_shard_visit_run: swap store needs the top %d bits outside the window", d->swap_g);
+    for (int c = 0; c < (1 << d->swap_g); ++c)
+      if (!d->out0[c] || (d->nv == 2 && !d->out1[c])) return invalid("qsb_shard_visit_run: missing swap target %d", c);
+  }
+  Runner R{ctx, t, n, false};
+  R.plus_amp = 1.0 / sqrt((double)(1ull << n_global));
+  R.maxgrid = (unsigned)std::min<uint64_t>(ctx->num_sms, 1ull << (n - kSweepT));
+  QSB_TRY(ensure_scratch(ctx, (uint64_t)2 * kSlots * R.maxgrid * sizeof(double) + 64));
+  R.partials = ctx->d_scratch;
+  const double2* lut = nullptr;
+  if ((d->flags & (QSB_SW_PRE_PHASE | QSB_SW_MID_PHASE)) && t->kind != 0) {
+    QSB_TRY(prepare_luts(t, {d->phase_scale}, {make_double2(1.0, 0.0)}, false));
+    lut = t->d_lut;
+  }
+  const Gate g1 = make_gate(d->theta1, false), g2 = make_gate(d->mode != SM_PLAIN ? d->theta2 : d->theta1, false);
+  const int pass2[2] = {d->lo2, d->hi2};
+  R.swap = d;
+  int idx = -1;
+  QSB_TRY(R.sweep_any(d->nv, d->mode, sh, d->mode != SM_PLAIN ? pass2 : nullptr, (double2*)v0, (double2*)v1, g1, g2,
+                      d->flags & ~QSB_SW_EXACT, lut, d->phase_scale, make_double2(1.0, 0.0), true, &idx));
+  std::vector<double> h;
+  QSB_TRY(R.fetch(h));
+  for (int k = 0; k < kSlots; ++k) sums[k] = Runner::slot_sum(h, R.maxgrid, R.grids, idx, k);
+  return QSB_OK;
+}
+
 }  // extern "C"
-
-namespace {
-
-}  // namespace
 
 extern "C" {
 

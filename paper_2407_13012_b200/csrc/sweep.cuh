@@ -80,7 +80,11 @@ struct SweepArgs {
   int form2;
   int mode;
   int groups;             // warp groups per CTA (1, or 2 for the R=5 single-vector family "6")
-  int want_pair;          // host: B sweeps may run as 2-CTA clusters (QSB_PAIR=1, fused.cu)
+  int want_pair;          // host: B sweeps may run as 2-CTA clusters (QSB_PAIR, fused.cu)
+  // fused qubit-swap store (sharded walk): the tile goes to sw_out[q][c], c = the tile's
+  // top sw_g local bits, at (local & (2^(sw_nl-sw_g)-1)) | (sw_rank << (sw_nl-sw_g))
+  int sw_g, sw_rank, sw_nl;
+  double2* sw_out[2][8];
   int pair;               // set at launch: this launch is paired (cluster barrier per tile)
   double* partials;       // [kSlots][gridDim.x]
   uint64_t ntiles;

@@ -561,10 +561,18 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     // MEMBAR then does not wait for this tile's 64 KB of stores to drain.
     if constexpr (NV == 1) fence_proxy_async();
     if (!(flags & SF_NO_STORE)) {
-      const uint64_t g1 = base + gofs<IS_A>(lb, glo);
+      uint64_t g1 = base + gofs<IS_A>(lb, glo);
+      double2* out[2] = {a.v0, a.v1};
+      if (a.sw_g) {  // qubit swap fused into the store: the whole tile goes to shard c
+        const int hb = a.sw_nl - a.sw_g;
+        const uint64_t c = base >> hb;
+        out[0] = a.sw_out[0][c];
+        out[1] = a.sw_out[1][c];
+        g1 = (g1 & ((1ull << hb) - 1ull)) | ((uint64_t)a.sw_rank << hb);
+      }
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
-        double2* dst = (q == 0 ? a.v0 : a.v1) + g1;
+        double2* dst = out[q] + g1;
 #pragma unroll
         for (int j = 0; j < NR; ++j) st_stream(dst + gofs<IS_A>((uint32_t)j << RL, glo), v[q][j]);
       }

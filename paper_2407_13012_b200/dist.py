@@ -118,13 +118,142 @@ def collect(steps, sums_per_step, p: int):
     return value, dg, db
 
 
+# ---------------------------------------------------------------- the window chain (fast mode)
+MID_PHASE, MID_DINNER, MID_EXPECT, XSUM2 = 512, 1024, 2048, 4096
+PLAIN, MERGED, BRIDGE = 0, 1, 2
+
+
+@dataclass(frozen=True)
+class Visit:
+    """One window visit on every shard (qsb_shard_visit, include/qsb.h)."""
+
+    nv: int
+    mode: int          # PLAIN / MERGED / BRIDGE
+    window: int        # 0: A window (bits 0..11), else a B window's first bit
+    lo1: int
+    hi1: int
+    theta1: float
+    lo2: int
+    hi2: int
+    theta2: float
+    flags: int
+    phase: float
+    swap: bool         # the qubit swap (layout A <-> B) follows this visit
+    routes: tuple      # (slot, kind, layer): kind 0 <C>, 1 d_gamma (x2), 2 d_beta (x-2)
+
+
+def shard_windows(n_l: int) -> list[tuple[int, int, int]]:
+    """Visit order of one layer's windows as (window, lo, hi): the top B window first
+    (it also takes the previous layer's g swapped-in qubits), the A window last (its
+    tiles hold fixed top bits, so the swap can follow -- or be fused into -- it)."""
+    if n_l < 21:
+        raise ContractViolation(f"the sharded chain needs >= 21 local qubits (n_l={n_l})")
+    wins = [(0, 0, 11)]
+    s = 12
+    while s <= n_l - 1:
+        glo = min(s, n_l - 9)
+        wins.append((glo, glo, glo + 8))
+        s += 9
+    order = list(reversed(wins))
+    out, covered = [], set()
+    for w, lo, hi in order:
+        pos = [q for q in range(lo, hi + 1) if q not in covered]
+        covered.update(pos)
+        if pos:
+            out.append((w, pos[0], pos[-1]))
+    return out
+
+
+def chain_program(n: int, g: int, gammas, betas, want_value: bool, want_grad: bool) -> list[Visit]:
+    """The sharded walk as window visits.  A layer gates its local positions window by
+    window (top B window, middle B windows, A window), then the top g local bits and
+    the rank bits trade places (one all-to-all, or fused into the A visit's store), and
+    the g qubits that arrived are gated in the next visit of the top window -- merged
+    with the next layer (phase between the passes), the bridge to the backward walk, or
+    a final tail.  Per layer: K visits + 1 swap (the per-position schedule of program()
+    needs K + 1 sweeps + 1 swap)."""
+    n_l = n - g
+    p = len(gammas)
+    wins = shard_windows(n_l)
+    top_w, top_lo, top_hi = wins[0]
+    arr_lo, arr_hi = n_l - g, n_l - 1
+    V = []
+    for i in range(p):
+        th = -2.0 * betas[i]
+        for k, (w, lo, hi) in enumerate(wins):
+            last = k == len(wins) - 1
+            if k == 0 and i == 0:
+                V.append(Visit(1, PLAIN, w, lo, hi, th, 0, 0, 0.0, PLUS | PRE_PHASE, -gammas[0], False, ()))
+            elif k == 0:
+                V.append(Visit(1, MERGED, w, arr_lo, arr_hi, -2.0 * betas[i - 1], lo, hi, th, MID_PHASE, -gammas[i],
+                               False, ()))
+            else:
+                V.append(Visit(1, PLAIN, w, lo, hi, th, 0, 0, 0.0, 0, 0.0, last, ()))
+    if not want_grad:
+        V.append(Visit(1, PLAIN, top_w, arr_lo, arr_hi, -2.0 * betas[p - 1], 0, 0, 0.0,
+                       POST_EXPECT if want_value else 0, 0.0, False, ((0, 0, 0),) if want_value else ()))
+        return V
+    for i in range(p - 1, -1, -1):
+        th = 2.0 * betas[i]
+        for k, (w, lo, hi) in enumerate(wins):
+            last = k == len(wins) - 1
+            if k == 0 and i == p - 1:
+                routes = ((3, 2, i),) + (((0, 0, 0),) if want_value else ())
+                V.append(Visit(2, BRIDGE, w, arr_lo, arr_hi, -2.0 * betas[p - 1], lo, hi, th,
+                               XSUM2 | (MID_EXPECT if want_value else 0), 0.0, False, routes))
+            elif k == 0:
+                V.append(Visit(2, MERGED, w, arr_lo, arr_hi, 2.0 * betas[i + 1], lo, hi, th,
+                               XSUM | MID_DINNER | MID_PHASE | XSUM2, gammas[i + 1], False,
+                               ((2, 2, i + 1), (1, 1, i + 1), (3, 2, i))))
+            else:
+                V.append(Visit(2, PLAIN, w, lo, hi, th, 0, 0, 0.0, XSUM, 0.0, last, ((2, 2, i),)))
+    V.append(Visit(2, PLAIN, top_w, arr_lo, arr_hi, 2.0 * betas[0], 0, 0, 0.0, XSUM | POST_DINNER | NO_STORE, 0.0,
+                   False, ((2, 2, 0), (0, 1, 0))))
+    return V
+
+
+def collect_chain(visits, sums, p: int):
+    value = None
+    dg = np.zeros(p)
+    db = np.zeros(p)
+    for v, s in zip(visits, sums):
+        for slot, kind, layer in v.routes:
+            if kind == 0:
+                value = s[slot]
+            elif kind == 1:
+                dg[layer] += 2.0 * s[slot]
+            else:
+                db[layer] += -2.0 * s[slot]
+    return value, dg, db
+
+
+class _ShardVisit(C.Structure):
+    _fields_ = [("nv", C.c_int), ("mode", C.c_int), ("window", C.c_int), ("lo1", C.c_int), ("hi1", C.c_int),
+                ("theta1", C.c_double), ("lo2", C.c_int), ("hi2", C.c_int), ("theta2", C.c_double),
+                ("flags", C.c_uint), ("phase_scale", C.c_double), ("swap_g", C.c_int), ("swap_rank", C.c_int),
+                ("out0", C.c_void_p * 8), ("out1", C.c_void_p * 8)]
+
+
 # ---------------------------------------------------------------- exchangers
 class VirtualExchanger:
     """All G shards live in this process on one device: the all-to-all is G^2 chunk copies."""
 
+    fused = True  # the swap is fused into the A visit's stores (shard buffers are plain device memory)
+
     def __init__(self, g: int):
         self.G = 1 << g
         self.ranks = list(range(self.G))
+
+    def setup(self, handle) -> None:
+        pass
+
+    def targets(self, name: str, spare: list[DeviceArray]) -> list[int]:
+        """where the fused swap store sends tile chunk c: shard c's spare buffer"""
+        return [b.ptr for b in spare]
+
+    def commit(self, name: str, live: list[DeviceArray], spare: list[DeviceArray]) -> None:
+        for k in range(len(live)):  # the spare buffers now hold the swapped state
+            live[k].ptr, spare[k].ptr = spare[k].ptr, live[k].ptr
 
     def combine(self, per_rank_sums: list[np.ndarray]) -> np.ndarray:
         total = np.zeros_like(per_rank_sums[0])
@@ -152,9 +281,17 @@ class VirtualExchanger:
 
 
 class TorchExchanger:
-    """One shard per process (torchrun): NCCL all-to-all over NVLink/NVSwitch."""
+    """One shard per process (torchrun).  The qubit swap is an NCCL all-to-all over
+    NVLink/NVSwitch after the A visit (default), or -- p2p=True / QSB_SHARD_P2P=1 -- fused
+    into the A visit's stores: every process opens its peers' spare buffers through CUDA
+    IPC and the sweep kernel writes each output tile straight into the shard that owns it
+    after the swap (NVLink P2P stores overlapped with the sweep; no separate pass).
+    With a gloo process group (tests: two processes on one GPU) the host-side
+    collectives run on CPU tensors."""
 
-    def __init__(self, g: int, dist, device: int):
+    def __init__(self, g: int, dist, device: int, p2p: bool | None = None):
+        import os
+
         self.G = 1 << g
         self.dist = dist
         self.rank = dist.get_rank()
@@ -162,11 +299,68 @@ class TorchExchanger:
         self.device = device
         if dist.get_world_size() != self.G:
             raise ContractViolation(f"world size {dist.get_world_size()} != 2^g = {self.G}")
+        if p2p is None:
+            p2p = os.environ.get("QSB_SHARD_P2P", "0") == "1"
+        self.fused = bool(p2p)
+        self.cpu = dist.get_backend() == "gloo"
+        self._peers: dict[str, list[list[int]]] = {}
+        self._parity: dict[str, int] = {}
+        self._opened: list[int] = []
+        self._ctx = None
+
+    def _tdev(self) -> str:
+        return "cpu" if self.cpu else f"cuda:{self.device}"
+
+    def setup(self, handle) -> None:
+        """P2P mode: export this shard's live/spare buffers, open every peer's."""
+        if not self.fused:
+            return
+        import torch
+
+        self._ctx = handle.ctx.device.handle
+        for name, (b0, b1) in (("ket", (handle.ket[0], handle.scratch[0])),
+                               ("bra", (handle.bra[0], handle.scratch_bra[0]))):
+            mine = np.zeros(128, dtype=np.uint8)
+            call("qsb_ipc_handle", self._ctx, b0.ptr, mine[:64].ctypes.data)
+            call("qsb_ipc_handle", self._ctx, b1.ptr, mine[64:].ctypes.data)
+            t = torch.as_tensor(mine, device=self._tdev())
+            out = [torch.empty_like(t) for _ in range(self.G)]
+            self.dist.all_gather(out, t)
+            ptrs = []
+            for r in range(self.G):
+                if r == self.rank:
+                    ptrs.append([b0.ptr, b1.ptr])
+                    continue
+                hb = np.ascontiguousarray(out[r].cpu().numpy())
+                pp = []
+                for off in (0, 64):
+                    p_ = C.c_void_p()
+                    call("qsb_ipc_open", self._ctx, hb[off:off + 64].ctypes.data, C.byref(p_))
+                    pp.append(p_.value)
+                    self._opened.append(p_.value)
+                ptrs.append(pp)
+            self._peers[name] = ptrs
+            self._parity[name] = 0
+
+    def targets(self, name: str, spare: list[DeviceArray]) -> list[int]:
+        par = self._parity[name]
+        return [self._peers[name][c][1 - par] for c in range(self.G)]
+
+    def commit(self, name: str, live: list[DeviceArray], spare: list[DeviceArray]) -> None:
+        call("qsb_device_sync", self._ctx)  # our stores into the peers are complete
+        self.dist.barrier()                  # ... and everybody's into ours
+        self._parity[name] ^= 1
+        live[0].ptr, spare[0].ptr = spare[0].ptr, live[0].ptr
+
+    def close(self) -> None:
+        for p_ in self._opened:
+            call("qsb_ipc_close", self._ctx, p_)
+        self._opened = []
 
     def combine(self, per_rank_sums: list[np.ndarray]) -> np.ndarray:
         import torch
 
-        mine = torch.tensor(per_rank_sums[0], dtype=torch.float64, device=f"cuda:{self.device}")
+        mine = torch.tensor(per_rank_sums[0], dtype=torch.float64, device=self._tdev())
         out = [torch.empty_like(mine) for _ in range(self.G)]
         self.dist.all_gather(out, mine)
         total = np.zeros_like(per_rank_sums[0])
@@ -177,7 +371,7 @@ class TorchExchanger:
     def gather(self, local: list[float]) -> list[float]:
         import torch
 
-        mine = torch.tensor(local, dtype=torch.float64, device=f"cuda:{self.device}")
+        mine = torch.tensor(local, dtype=torch.float64, device=self._tdev())
         out = [torch.empty_like(mine) for _ in range(self.G)]
         self.dist.all_gather(out, mine)
         return [float(x) for t in out for x in t.cpu().tolist()]
@@ -187,7 +381,7 @@ class TorchExchanger:
 
         res = []
         for a in arrays:  # exactly one rank contributes each entry: the sum is exact
-            t = torch.as_tensor(a, device=f"cuda:{self.device}")
+            t = torch.as_tensor(a, device=self._tdev())
             self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
             res.append(t.cpu().numpy())
         return tuple(res)
@@ -195,6 +389,8 @@ class TorchExchanger:
     def swap(self, vecs: list[DeviceArray], scratch: list[DeviceArray]) -> None:
         import torch
 
+        if self.fused:
+            raise ContractViolation("the P2P exchanger swaps inside the sweeps (fast-mode window chain only)")
         v, s = vecs[0], scratch[0]
         v.dctx.sync()  # our stream -> NCCL's stream
         src = torch.as_tensor(_CudaView(v), device=f"cuda:{self.device}").view(self.G, -1)
@@ -243,6 +439,11 @@ class ShardedHandle:
         self.ket = [DeviceArray(dctx, N_l, np.complex128) for _ in self.ranks]
         self.bra = [DeviceArray(dctx, N_l, np.complex128) for _ in self.ranks]
         self.scratch = [DeviceArray(dctx, N_l, np.complex128) for _ in self.ranks]
+        # the fused swap of a bra/ket visit needs a second spare buffer (allocated lazily,
+        # up front for P2P so it can be exported)
+        self.scratch_bra = None
+        if exchanger.fused and not isinstance(exchanger, VirtualExchanger):
+            self.scratch_bra = [DeviceArray(dctx, N_l, np.complex128) for _ in self.ranks]
         w = np.ascontiguousarray(poly.weights, dtype=np.float64)
         m = np.ascontiguousarray(poly.masks, dtype=np.int64)
         self.tables = [[None] * len(self.ranks), [None] * len(self.ranks)]
@@ -259,13 +460,14 @@ class ShardedHandle:
                 lo, hi = min(lo, mn.value), max(hi, mx.value)
         self.min_value, self.max_value = self._minmax(lo, hi)
         self.layout = 0
+        exchanger.setup(self)
 
     def _minmax(self, lo: float, hi: float) -> tuple[float, float]:
         if isinstance(self.ex, VirtualExchanger):
             return lo, hi
         import torch
 
-        t = torch.tensor([-lo, hi], dtype=torch.float64, device=f"cuda:{self.ex.device}")
+        t = torch.tensor([-lo, hi], dtype=torch.float64, device=self.ex._tdev())
         self.ex.dist.all_reduce(t, op=self.ex.dist.ReduceOp.MAX)
         return -float(t[0]), float(t[1])
 
@@ -300,9 +502,57 @@ class ShardedHandle:
         self.layout = layout
         return out
 
+    def _use_chain(self, exact: bool) -> bool:
+        import os
+
+        return not exact and self.n_l >= 21 and os.environ.get("QSB_SHARD_CHAIN", "1") != "0"
+
+    def _run_chain(self, visits: list[Visit]) -> list[np.ndarray]:
+        """Execute the window chain on this process's shards (fast mode)."""
+        h = self.ctx.device.handle
+        layout = self.layout
+        per_visit = []
+        for v in visits:
+            fused = v.swap and self.ex.fused
+            if fused and v.nv == 2 and self.scratch_bra is None:
+                self.scratch_bra = [DeviceArray(self.ctx.device, 1 << self.n_l, np.complex128) for _ in self.ranks]
+            per = []
+            for k, r in enumerate(self.ranks):
+                d = _ShardVisit(v.nv, v.mode, v.window, v.lo1, v.hi1, v.theta1, v.lo2, v.hi2, v.theta2, v.flags,
+                                v.phase, self.g if fused else 0, r)
+                if fused:
+                    for c, ptr in enumerate(self.ex.targets("ket", self.scratch)):
+                        d.out0[c] = ptr
+                    if v.nv == 2:
+                        for c, ptr in enumerate(self.ex.targets("bra", self.scratch_bra)):
+                            d.out1[c] = ptr
+                out = (C.c_double * 4)()
+                call("qsb_shard_visit_run", h, self.tables[layout][k].table.ptr, self.ket[k].ptr,
+                     self.bra[k].ptr if v.nv == 2 else None, self.n_l, self.n, C.byref(d), out)
+                per.append(np.array(out[:4]))
+            per_visit.append(per)
+            if v.swap:
+                if fused:
+                    self.ex.commit("ket", self.ket, self.scratch)
+                    if v.nv == 2:
+                        self.ex.commit("bra", self.bra, self.scratch_bra)
+                else:
+                    self.ex.swap(self.ket, self.scratch)
+                    if v.nv == 2:
+                        self.ex.swap(self.bra, self.scratch)
+                layout ^= 1
+        stacked = [np.concatenate([pv[k] for pv in per_visit]) for k in range(len(self.ranks))]
+        total = self.ex.combine(stacked)
+        self.layout = layout
+        return [total[4 * j: 4 * j + 4] for j in range(len(visits))]
+
     def value_and_grad(self, params: circuit.QaoaParams, exact: bool = False):
         if params.p < 1:
             raise ContractViolation("gradient needs depth p >= 1")
+        if self._use_chain(exact):
+            visits = chain_program(self.n, self.g, params.gammas, params.betas, True, True)
+            value, dg, db = collect_chain(visits, self._run_chain(visits), params.p)
+            return self._clamp(value), dg, db
         steps = program(self.n, self.g, params.gammas, params.betas, True, True)
         value, dg, db = collect(steps, self._run(steps, exact), params.p)
         return self._clamp(value), dg, db
@@ -310,6 +560,10 @@ class ShardedHandle:
     def expectation(self, params: circuit.QaoaParams, exact: bool = False) -> float:
         if params.p < 1:
             raise ContractViolation("sharded expectation needs p >= 1")
+        if self._use_chain(exact):
+            visits = chain_program(self.n, self.g, params.gammas, params.betas, True, False)
+            value, _, _ = collect_chain(visits, self._run_chain(visits), params.p)
+            return self._clamp(value)
         steps = program(self.n, self.g, params.gammas, params.betas, True, False)
         value, _, _ = collect(steps, self._run(steps, exact), params.p)
         return self._clamp(value)
@@ -383,10 +637,15 @@ class ShardedHandle:
         return sampling.SampleSet(shots=shots, seed=seed, indices=idx, costs=cost)
 
     def simulate(self, params: circuit.QaoaParams, exact: bool = False) -> None:
+        if self._use_chain(exact) and params.p >= 1:
+            self._run_chain(chain_program(self.n, self.g, params.gammas, params.betas, False, False))
+            return
         steps = program(self.n, self.g, params.gammas, params.betas, False, False)
         self._run(steps, exact)
 
     def close(self) -> None:
-        for arrs in (self.ket, self.bra, self.scratch, *self.tables):
+        if hasattr(self.ex, "close"):
+            self.ex.close()
+        for arrs in (self.ket, self.bra, self.scratch, self.scratch_bra or [], *self.tables):
             for a in arrs:
                 a.free()

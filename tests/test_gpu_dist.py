@@ -84,3 +84,59 @@ def test_sharded_draw_matches_the_unsharded_tree(n, g):
     assert np.array_equal(ss.costs, cost)
     assert sh.layout == 0
     sh.close()
+
+
+@pytest.mark.parametrize("n,g,p", [(22, 1, 2), (23, 2, 3), (24, 3, 2), (26, 1, 1)])
+def test_sharded_window_chain(n, g, p, monkeypatch):
+    """fast-mode sharded walk as a window chain (dist.chain_program): merged visits at
+    the top window, the qubit swap fused into the A visit's stores (virtual shards:
+    stores straight into the other shards' buffers) -- against the per-position
+    schedule (QSB_SHARD_CHAIN=0) and the unsharded single-GPU chain"""
+    poly = random_instance(60 + n, n)
+    params = random_params(n + 9, p)
+    sh = dist.ShardedHandle(poly, g, dist.VirtualExchanger(g))
+    v1, dg1, db1 = sh.value_and_grad(params)
+    e1 = sh.expectation(params)
+    sh.simulate(params)
+    st1 = sh.gather_state()
+    monkeypatch.setenv("QSB_SHARD_CHAIN", "0")
+    v0, dg0, db0 = sh.value_and_grad(params)
+    sh.simulate(params)
+    st0 = sh.gather_state()
+    sh.close()
+    h = qs.create_handle(poly, backend_name="b200")
+    v2, g2 = qs.value_and_grad(h, params)
+    h.close()
+    assert abs(v1 - v0) <= 1e-11 * max(1.0, abs(v0)) and abs(v1 - v2) <= 1e-11 * max(1.0, abs(v2))
+    assert abs(e1 - v1) <= 1e-11 * max(1.0, abs(v1))
+    ref = np.concatenate([np.array(g2.d_gammas), np.array(g2.d_betas)])
+    assert rel_err(np.concatenate([dg1, db1]), ref) <= 1e-10
+    assert rel_err(np.concatenate([dg1, db1]), np.concatenate([dg0, db0])) <= 1e-11
+    assert rel_err(st1, st0) <= 1e-12
+
+
+def test_two_process_p2p_swap(tmp_path):
+    """Two processes, one shard each, the qubit swap fused into the A visit's stores
+    through CUDA IPC (QSB_SHARD_P2P path of dist.TorchExchanger) -- both on the one GPU
+    here; equals the single-process virtual-shard run."""
+    import os
+    import subprocess
+    import sys
+
+    n, p = 22, 2
+    out = tmp_path / "res.npz"
+    env = dict(os.environ, QSB_SHARD_P2P="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29531",
+           os.path.join(os.path.dirname(__file__), "mp_shard_worker.py"), str(out), str(n), str(p)]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    got = np.load(out)
+    poly = random_instance(70 + n, n)
+    params = random_params(n + 3, p)
+    sh = dist.ShardedHandle(poly, 1, dist.VirtualExchanger(1))
+    v, dg, db = sh.value_and_grad(params)
+    sh.close()
+    assert abs(float(got["v"]) - v) <= 1e-12 * max(1.0, abs(v))
+    assert abs(float(got["e"]) - v) <= 1e-11 * max(1.0, abs(v))
+    assert rel_err(np.concatenate([got["dg"], got["db"]]), np.concatenate([dg, db])) <= 1e-12
