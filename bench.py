@@ -46,8 +46,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--n", type=int, default=N_QUBITS)
-    ap.add_argument("--p", type=int, default=DEPTH)
+    # (--qubits / --depth: unambiguous under torch.distributed.run, which takes --n... itself)
+    ap.add_argument("--n", "--qubits", dest="n", type=int, default=N_QUBITS)
+    ap.add_argument("--p", "--depth", dest="p", type=int, default=DEPTH)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--params", choices=["ramp", "random"], default="ramp")
     ap.add_argument("--shots", type=int, default=1_000_000)
@@ -290,7 +291,8 @@ def run_sharded(args, rank: int, world: int, dist) -> None:
     g = world.bit_length() - 1
     if 1 << g != world:
         raise SystemExit("sharded bench needs a power-of-two GPU count")
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+    tdev = "cpu" if dist.get_backend() == "gloo" else f"cuda:{local}"
     n = args.n if args.n != N_QUBITS else N_QUBITS + g
     poly, params = workload(n, args.p, args.params)
     # the qubit swap fused into the sweeps' stores over NVLink (CUDA IPC peer buffers);
@@ -319,7 +321,7 @@ def run_sharded(args, rank: int, world: int, dist) -> None:
         ev1.synchronize()
     ms = ev0.elapsed_time(ev1)
     launches = dev.launches() - launches0
-    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([ms], dtype=torch.float64, device=tdev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     if rank == 0:
@@ -423,7 +425,8 @@ def run_b200(args, rank: int, world: int, dist) -> None:
     if dist is not None:
         import torch
 
-        t = torch.tensor([ms, wall_ms, sim_ms], dtype=torch.float64, device=f"cuda:{dev.device}")
+        tdev = "cpu" if dist.get_backend() == "gloo" else f"cuda:{dev.device}"
+        t = torch.tensor([ms, wall_ms, sim_ms], dtype=torch.float64, device=tdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, wall_ms, sim_ms = (float(x) for x in t.tolist())
     if rank != 0:
@@ -508,7 +511,12 @@ def main():
         import torch
         import torch.distributed as tdist
 
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        # QSB_BENCH_DIST_BACKEND / QSB_BENCH_SAME_GPU=1: smoke-test the N>1 paths with
+        # several processes on one GPU (gloo host collectives; NCCL needs distinct GPUs)
+        backend = os.environ.get("QSB_BENCH_DIST_BACKEND", "nccl" if torch.cuda.is_available() else "gloo")
+        if os.environ.get("QSB_BENCH_SAME_GPU") == "1":
+            local = 0
+            os.environ["LOCAL_RANK_DEVICE"] = "0"
         if backend == "nccl":
             torch.cuda.set_device(local)
         tdist.init_process_group(backend=backend)
