@@ -140,3 +140,27 @@ def test_two_process_p2p_swap(tmp_path):
     assert abs(float(got["v"]) - v) <= 1e-12 * max(1.0, abs(v))
     assert abs(float(got["e"]) - v) <= 1e-11 * max(1.0, abs(v))
     assert rel_err(np.concatenate([got["dg"], got["db"]]), np.concatenate([dg, db])) <= 1e-12
+
+
+def test_sharded_chain_float_table_and_sampling():
+    """window chain with an f64 table (device sincos between the passes) and a draw
+    from the chain-simulated sharded state"""
+    n, g, p = 22, 1, 2
+    rs = np.random.default_rng(5)
+    terms = [((rs.random() - 0.5) * 6.0, 1 << i) for i in range(n)]
+    terms += [((rs.random() - 0.5) * 6.0, (1 << i) | (1 << j)) for i in range(n) for j in range(i + 1, n)
+              if rs.random() < 0.3]
+    poly = qs.Polynomial(n, terms)
+    params = random_params(12, p)
+    sh = dist.ShardedHandle(poly, g, dist.VirtualExchanger(g))
+    v, dg, db = sh.value_and_grad(params)
+    table = oracle.precompute_table(poly.weights, poly.masks, n)
+    e, wdg, wdb = oracle.value_and_grad(table, n, params.gammas, params.betas)
+    assert abs(v - e) <= 1e-10 * max(1.0, abs(e))
+    assert rel_err(np.concatenate([dg, db]), np.concatenate([wdg, wdb])) <= 1e-10
+    sh.simulate(params)
+    state = sh.gather_state()
+    ss = sh.draw(5000, 3)
+    idx, cost = oracle.sample(state, table, 5000, 3)
+    assert np.array_equal(ss.indices, idx) and np.array_equal(ss.costs, cost)
+    sh.close()
