@@ -361,6 +361,51 @@ def run_sharded(args, rank: int, world: int, dist) -> None:
     sh.close()
 
 
+def small_configs() -> dict:
+    """BASELINE.json configs 1-2 through the public API (wall clock per call, median of
+    repeats; the C3 handle is closed by then): C1 reg3 n=16 p=3 (+1024 shots), C2 ER(24,0.5)
+    p=4 with the adjoint gradient over all 8 angles."""
+    import paper_2407_13012_b200 as qs
+
+    out = {}
+
+    def med(fn, reps):
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return 1e3 * statistics.median(ts)
+
+    g1 = qs.maxcut_polynomial(qs.random_regular(16, 3, seed=1))
+    h1 = qs.create_handle(g1, backend_name="b200")
+    p1 = qs.linear_ramp_params(3)
+    qs.value_and_grad(h1, p1)
+    out["C1_reg3_n16_p3"] = {
+        "expectation_ms": med(lambda: qs.expectation(h1, p1), 20),
+        "value_and_grad_ms": med(lambda: qs.value_and_grad(h1, p1), 20),
+        "sample_1024_ms": med(lambda: qs.sample(h1, p1, 1024, 1), 20),
+        "expectation": qs.expectation(h1, p1),
+    }
+    h1.close()
+    g2 = qs.maxcut_polynomial(qs.erdos_renyi(24, 0.5, seed=1))
+    t0 = time.perf_counter()
+    h2 = qs.create_handle(g2, backend_name="b200")
+    h2.ctx.synchronize()
+    pre = 1e3 * (time.perf_counter() - t0)
+    p2 = qs.linear_ramp_params(4)
+    qs.value_and_grad(h2, p2)
+    out["C2_er24_p4"] = {
+        "precompute_ms": pre,
+        "gradient_ms": med(lambda: qs.gradient(h2, p2), 10),
+        "value_and_grad_ms": med(lambda: qs.value_and_grad(h2, p2), 10),
+        "expectation": qs.expectation(h2, p2),
+        "reference_numba_s": {"gradient": 5.63, "source": "BASELINE.md section 3 (8-core survey container)"},
+    }
+    h2.close()
+    return out
+
+
 def run_b200(args, rank: int, world: int, dist) -> None:
     import numpy as np
 
@@ -490,6 +535,9 @@ def run_b200(args, rank: int, world: int, dist) -> None:
         },
         "clocks": clk.summary(),
     }
+    h.close()
+    if world == 1 and args.n == N_QUBITS:
+        line["other_configs"] = small_configs()
     if world == 1 and not args.no_cpu_baseline:
         info = cpu_reference_step(args.n, args.p)
         line["cpu_baseline"] = {
@@ -497,7 +545,6 @@ def run_b200(args, rank: int, world: int, dist) -> None:
             "sample": f"reference op sequence for one E+grad (p={args.p}) composed from each oracle primitive timed "
                       f"once at n={info['n_cpu']} ({info['sampled_seconds']:.1f} s CPU), scaled to n={args.n}",
         }
-    h.close()
     print(json.dumps(line), flush=True)
 
 
