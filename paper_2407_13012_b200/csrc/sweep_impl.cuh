@@ -40,7 +40,14 @@ constexpr int kRing = 3;  // shared-memory slots (one vector-tile each)
 constexpr uint32_t kTile = 1u << kSweepT;
 constexpr uint32_t kSlotBytes = kTile * 16u;
 constexpr uint32_t kCBytes = kTile * 2u;  // compact-index slot (u16 worst case)
-constexpr size_t kSmemBytes = (size_t)kRing * kSlotBytes + (size_t)kRing * kCBytes + 256 * 16 + 64;
+// u8 phase LUT: up to kLutRep entries are stored 8 times interleaved (entry e, copy q at
+// 8e + q) and lane q of each 8-lane quarter-warp reads copy q, so a 16-byte LUT load is
+// conflict-free whatever the entries; larger LUTs (<= 256 entries) are stored once.
+constexpr int kLutRep = 80;
+constexpr uint32_t kLutBytes = kLutRep * 8 * 16;  // 10 KB (the 227 KB budget: ring + index ring + LUT + barriers)
+constexpr size_t kSmemBytes = (size_t)kRing * kSlotBytes + (size_t)kRing * kCBytes + kLutBytes + 64;
+static_assert(kSmemBytes <= 232448, "dynamic shared memory per block on sm_100");
+static_assert(256 * 16 <= kLutBytes, "a plain LUT of 256 entries must fit");
 
 __host__ __device__ constexpr uint32_t swz(uint32_t x) {
   return x ^ (((x >> 3) ^ (x >> 6) ^ (x >> 9) ^ (x >> 12)) & 7u);
@@ -208,7 +215,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
   const uint32_t cring_s = ring_s + kRing * kSlotBytes;
   uint8_t* cring = smem_raw + kRing * kSlotBytes;
   double2* slut = (double2*)(cring + kRing * kCBytes);
-  const uint32_t bar_s = ring_s + kRing * kSlotBytes + kRing * kCBytes + 256 * 16;
+  const uint32_t bar_s = ring_s + kRing * kSlotBytes + kRing * kCBytes + kLutBytes;
 
   const int tid = threadIdx.x & (NT - 1), grp = GR == 1 ? 0 : (int)(threadIdx.x / NT);
   const int lane = tid & 31, warp = tid >> 5;  // within the group
@@ -224,7 +231,11 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (!KSIN && a.kind == 1 && (flags & (SF_PRE_PHASE | SF_MID_PHASE))) {  // u8 LUT in smem
-    for (int i = threadIdx.x; i < a.nlut; i += GR * NT) slut[i] = a.lut[i];
+    if (a.nlut <= kLutRep) {
+      for (int i = threadIdx.x; i < 8 * a.nlut; i += GR * NT) slut[i] = a.lut[i >> 3];
+    } else {
+      for (int i = threadIdx.x; i < a.nlut; i += GR * NT) slut[i] = a.lut[i];
+    }
   }
   __syncthreads();
 
@@ -356,12 +367,15 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
         return f;
       }
     };
+    // LUT slot of entry c: replicated (8c + lane%8) or plain (c)
+    const uint32_t lrep = a.nlut <= kLutRep ? 3u : 0u, lq = a.nlut <= kLutRep ? (uint32_t)(lane & 7) : 0u;
     struct TvU8 {  // u8 index tile in natural order, LUT in smem
       const SweepArgs& a;
       const uint8_t* cs;
       const double2* slut;
+      uint32_t lrep, lq;
       __device__ double val(uint32_t l, uint64_t) const { return a.vmin + (double)cs[l]; }
-      __device__ double2 phase(uint32_t l, uint64_t) const { return slut[cs[l]]; }
+      __device__ double2 phase(uint32_t l, uint64_t) const { return slut[((uint32_t)cs[l] << lrep) | lq]; }
     };
     struct TvU16 {  // u16 index tile, LUT in HBM (L1-cached)
       const SweepArgs& a;
@@ -373,18 +387,18 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
       const SweepArgs& a;
       const uint8_t* cs;
       const double2* slut;
-      uint32_t tb8;
+      uint32_t tb8, lrep, lq;
       __device__ uint32_t at(uint32_t l) const { return ((l >> 3) << 4) | tb8 | (l & 7u); }
       __device__ double val(uint32_t l, uint64_t) const { return a.vmin + (double)cs[at(l)]; }
-      __device__ double2 phase(uint32_t l, uint64_t) const { return slut[cs[at(l)]]; }
+      __device__ double2 phase(uint32_t l, uint64_t) const { return slut[((uint32_t)cs[at(l)] << lrep) | lq]; }
     };
     // table-kind dispatch hoisted out of the unrolled loops (tv: value / phase views)
     auto with_table = [&](auto&& fn) {
       if constexpr (KSIN) {
         fn(TvF64{a});
       } else {
-        if (cmode == 2) fn(TvU8Rows{a, cs, slut, tb8});
-        else if (a.kind == 1) fn(TvU8{a, cs, slut});
+        if (cmode == 2) fn(TvU8Rows{a, cs, slut, tb8, lrep, lq});
+        else if (a.kind == 1) fn(TvU8{a, cs, slut, lrep, lq});
         else if (a.kind == 2) fn(TvU16{a, (const uint16_t*)cs});
         else fn(TvF64{a});
       }
