@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(256, 1) k_btile(const __grid_constant__ CUtens
 // Generalised A-window probe: NV vectors (2: bra/ket with slots 2k%3 / (2k+1)%3 as in
 // the library), MERGED = two gate passes (phases 0,1,2 then 2,1,0), XSUM = bra/ket
 // contraction after each phase's gates.
-template <int NV, bool MERGED, int XSUM, int MID = 0>
+template <int NV, bool MERGED, int XSUM, int MID = 0, bool STAG = false>
 __global__ void __launch_bounds__(256, 1) k_probe(double2* __restrict__ v0g, double2* __restrict__ v1g, uint64_t ntiles,
                                                    double gb, double* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(256, 1) k_probe(double2* __restrict__ v0g, dou
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[q][j] = lds((q == 0 ? sk : sb) + swz(pb | (j << P.reg)) * 16u);
     };
-    auto gates = [&]() {
+    auto gates = [&](int q0 = 0, int q1 = NV, bool xs = true) {
       double x[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) x[i] = 0.0;
@@ -308,9 +308,10 @@ __global__ void __launch_bounds__(256, 1) k_probe(double2* __restrict__ v0g, dou
         for (int j = 0; j < 16; ++j)
           if (!(j & (1 << b))) {
 #pragma unroll
-            for (int q = 0; q < NV; ++q) bfly(v[q][j], v[q][j | (1 << b)], gb);
+            for (int q = 0; q < NV; ++q)
+              if (q >= q0 && q < q1) bfly(v[q][j], v[q][j | (1 << b)], gb);
           }
-      if (XSUM && NV == 2) {  // after the gates (X_j commutes with the layer)
+      if (XSUM && NV == 2 && xs) {  // after the gates (X_j commutes with the layer)
 #pragma unroll
         for (int b = 0; b < 4; ++b)
 #pragma unroll
@@ -327,11 +328,32 @@ __global__ void __launch_bounds__(256, 1) k_probe(double2* __restrict__ v0g, dou
         for (int i = 0; i < 8; ++i) acc += x[i];
       }
     };
+    // staggered exchange (NV=2): the ket's loads and gates overlap the bra's stores
+    auto xg = [&](int qi, int pi) {
+      if (!STAG || NV != 2) {
+        exch(qi, pi);
+        gates();
+        return;
+      }
+      const Map Q = map_of(qi), P = map_of(pi);
+      const uint32_t qb = mbase(Q, lane, warp), pb = mbase(P, lane, warp);
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) sts(sk + swz(qb | (j << Q.reg)) * 16u, v[0][j]);
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[0][j] = lds(sk + swz(pb | (j << P.reg)) * 16u);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) sts(sb + swz(qb | (j << Q.reg)) * 16u, v[NV - 1][j]);
+      gates(0, 1, false);
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[NV - 1][j] = lds(sb + swz(pb | (j << P.reg)) * 16u);
+      gates(1, 2, true);
+    };
     gates();
-    exch(0, 1);
-    gates();
-    exch(1, 2);
-    gates();
+    xg(0, 1);
+    xg(1, 2);
     int last = 2;
     if (MERGED && MID) {
       const uint32_t lm = mbase(map_of(2), lane, warp);
@@ -348,10 +370,8 @@ __global__ void __launch_bounds__(256, 1) k_probe(double2* __restrict__ v0g, dou
       }
     }
     if (MERGED) {
-      exch(2, 1);
-      gates();
-      exch(1, 0);
-      gates();
+      xg(2, 1);
+      xg(1, 0);
       last = 0;
     }
     if (NV == 2) {
@@ -522,11 +542,14 @@ int main() {
   setp(k_probe<1, true, 0, 1>);
   setp(k_probe<2, true, 3, 2>);
   setp(k_probe<1, true, 0, 2>);
+  setp(k_probe<2, true, 3, 1, true>);
+  setp(k_probe<2, false, 3, 0, true>);
   const char* pnames[] = {"probe A NV1 plain", "probe A NV1 merged", "probe A NV2 plain", "probe A NV2 plain+xsum(1 acc)",
                           "probe A NV2 plain+xsum(4 acc)", "probe A NV2 plain+xsum(8 acc)", "probe A NV2 merged",
-                          "probe A NV2 merged+xsum(8 acc)", "probe A NV2 merged+xsum+mid", "probe A NV1 merged+mid", "probe A NV2 merged+xsum+mid(pf)", "probe A NV1 merged+mid(pf)"};
-  const double pbytes[] = {32.0, 32.0, 64.0, 64.0, 64.0, 64.0, 64.0, 64.0, 64.0, 32.0, 64.0, 32.0};
-  for (int m = 0; m < 12; ++m) {
+                          "probe A NV2 merged+xsum(8 acc)", "probe A NV2 merged+xsum+mid", "probe A NV1 merged+mid", "probe A NV2 merged+xsum+mid(pf)", "probe A NV1 merged+mid(pf)",
+                          "probe A NV2 merged+xsum+mid STAGGERED", "probe A NV2 plain+xsum STAGGERED"};
+  const double pbytes[] = {32.0, 32.0, 64.0, 64.0, 64.0, 64.0, 64.0, 64.0, 64.0, 32.0, 64.0, 32.0, 64.0, 64.0};
+  for (int m = 0; m < 14; ++m) {
     float best = 1e9f;
     for (int rep = 0; rep < 5; ++rep) {
       cudaEventRecord(e0);
@@ -542,6 +565,8 @@ int main() {
       if (m == 9) k_probe<1, true, 0, 1><<<sms, 256, smem>>>(a, b, ntiles, 0.3, dout);
       if (m == 10) k_probe<2, true, 3, 2><<<sms, 256, smem>>>(a, b, ntiles, 0.3, dout);
       if (m == 11) k_probe<1, true, 0, 2><<<sms, 256, smem>>>(a, b, ntiles, 0.3, dout);
+      if (m == 12) k_probe<2, true, 3, 1, true><<<sms, 256, smem>>>(a, b, ntiles, 0.3, dout);
+      if (m == 13) k_probe<2, false, 3, 0, true><<<sms, 256, smem>>>(a, b, ntiles, 0.3, dout);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
