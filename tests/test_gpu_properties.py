@@ -76,3 +76,25 @@ def test_norm_bounds_and_consistency(n, p, seed):
     assert abs(np.vdot(psi, psi).real - 1.0) <= 1e-12
     assert lo <= e <= hi
     assert abs(v - e) <= 1e-12 * max(1.0, abs(e))
+
+
+def test_concurrent_handles_from_threads():
+    """distinct handles may run concurrently (the reference's bench --jobs
+    uses a thread pool): one CUDA stream per context, ctypes drops the GIL -- results
+    equal the sequential ones bit for bit"""
+    from concurrent.futures import ThreadPoolExecutor
+
+    cases = [(random_instance(600 + k, n), n) for k, n in enumerate((9, 14, 17, 20, 12, 16))]
+    params = qs.QaoaParams([0.4, -0.2], [0.7, 0.1])
+
+    def run(case):
+        poly, _ = case
+        h = qs.create_handle(poly, backend_name="b200")
+        out = [qs.value_and_grad(h, params) for _ in range(3)]
+        h.close()
+        return [(v, tuple(flat(g))) for v, g in out]
+
+    seq = [run(c) for c in cases]
+    with ThreadPoolExecutor(max_workers=6) as pool:
+        par = list(pool.map(run, cases))
+    assert par == seq
