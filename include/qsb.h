@@ -191,6 +191,14 @@ int qsb_layer_sweeps(qsb_ctx* ctx, qsb_table* t, double* v0, double* v1, int nv,
  * Im<bra|C|ket>, 2 xsum of pass 1, 3 xsum of pass 2}.  n = local qubits of the shard. */
 int qsb_shard_visit_run(qsb_ctx* ctx, qsb_table* t, double* v0, double* v1, int n, int n_global,
                         const qsb_shard_visit* d, double* sums);
+/* Many small registers (n <= 11 each) in ONE launch, one CTA per instance (the
+ * paper's many-graphs regime; no reference counterpart -- the reference runs handles
+ * one by one, cli.py bench --jobs).  Instance k: table tables[k], state kets[k]
+ * (written with the final ket), depth ps[k], angles gammas/betas concatenated in
+ * instance order.  mode 0 simulate, 1 + <C>, 2 + gradient.  out (host): per instance
+ * 1 + 2p doubles: <C> (unclamped), d_gamma[p], d_beta[p]. */
+int qsb_small_batch(qsb_ctx* ctx, int count, qsb_table* const* tables, double* const* kets, const int* ps,
+                    const double* gammas, const double* betas, int mode, double* out);
 /* <psi|C|psi> (circuit.expectation_of_state, circuit.py:106-113, without the clamp) */
 int qsb_expectation(qsb_ctx* ctx, qsb_table* t, const double* amps, unsigned flags, double* out);
 /* expectation + adjoint gradient (adjoint.py:37-77): one forward, one backward walk

@@ -89,6 +89,7 @@ _SIGS = {
     "qsb_ipc_open": [_vp, _vp, C.POINTER(_vp)],
     "qsb_ipc_close": [_vp, _vp],
     "qsb_device_sync": [_vp],
+    "qsb_small_batch": [_vp, _i32, _vp, _vp, _vp, _dp, _dp, _i32, _dp],
     "qsb_sample_descend": [_vp, _vp, _vp, _i32, _u64, _vp, _vp, _vp],
 }
 _RESTYPES = {"qsb_last_error": C.c_char_p, "qsb_abi_version": _i32}

@@ -61,7 +61,7 @@ __device__ double block_tree(double v[kSPer], double* wsum) {
   return w8[0];  // every thread holds the root
 }
 
-__global__ void __launch_bounds__(kST, 1) k_small(const SmallArgs a) {
+__device__ __forceinline__ void small_body(const SmallArgs& a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   double2* ket = (double2*)smem_raw;
   double2* bra = ket + kSMax;
@@ -171,6 +171,17 @@ __global__ void __launch_bounds__(kST, 1) k_small(const SmallArgs a) {
   for (int i = tid; i < N; i += kST) a.ket[i] = ket[i];
 }
 
+__global__ void __launch_bounds__(kST, 1) k_small(const SmallArgs a) { small_body(a); }
+
+// batched: one CTA per (handle, parameters) instance -- the paper's many-small-graphs
+// regime (444-graph suite, optimizer restarts) in one launch
+__global__ void __launch_bounds__(kST, 1) k_small_batch(const SmallArgs* __restrict__ args) {
+  const SmallArgs a = args[blockIdx.x];
+  small_body(a);
+}
+
+constexpr size_t kSmallSmem = (size_t)kSMax * (16 + 16 + 8) + 2 * (kST / 32) * sizeof(double);
+
 }  // namespace
 
 namespace qsb {
@@ -222,7 +233,7 @@ int small_run(qsb_ctx* ctx, qsb_table* t, double2* ket, int p, const double* gam
   a.nvals = t->nvals;
   a.mode = mode;
   a.want_value = value != nullptr;
-  const size_t smem = (size_t)kSMax * (16 + 16 + 8) + 2 * (kST / 32) * sizeof(double);
+  const size_t smem = kSmallSmem;
   static bool attr = false;
   if (!attr) {
     QSB_CUDA(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -246,3 +257,95 @@ int small_run(qsb_ctx* ctx, qsb_table* t, double2* ket, int p, const double* gam
 }
 
 }  // namespace qsb
+
+extern "C" {
+
+// Many small registers in one launch (see qsb.h).  Host work per instance: Rx (c, s)
+// and phase LUT / angles, all packed into one upload.
+int qsb_small_batch(qsb_ctx* ctx, int count, qsb_table* const* tables, double* const* kets, const int* ps,
+                    const double* gammas, const double* betas, int mode, double* out) {
+  if (!ctx || count < 0 || (count > 0 && (!tables || !kets || !ps || !gammas || !betas || !out)))
+    return invalid("qsb_small_batch: null argument");
+  if (mode < 0 || mode > 2) return invalid("qsb_small_batch: mode must be 0 (simulate), 1 (+<C>) or 2 (+gradient)");
+  if (count == 0) return QSB_OK;
+  // host staging: per instance [rxcs 4p][ang 2p][lut 2p*nvals*2]; outputs 1 + 2p
+  std::vector<size_t> off(count + 1, 0), ooff(count + 1, 0), poff(count + 1, 0);
+  for (int k = 0; k < count; ++k) {
+    const qsb_table* t = tables[k];
+    if (!t || !kets[k]) return invalid("qsb_small_batch: instance %d has no table / state", k);
+    if (t->n < 1 || t->n > 11) return invalid("qsb_small_batch: instance %d has n=%d (1..11)", k, t->n);
+    if (ps[k] < 1) return invalid("qsb_small_batch: instance %d has p=%d", k, ps[k]);
+    const size_t nv = t->kind != 0 ? (size_t)t->nvals : 0;
+    off[k + 1] = off[k] + 6 * (size_t)ps[k] + 4 * (size_t)ps[k] * nv;
+    ooff[k + 1] = ooff[k] + 1 + 2 * (size_t)ps[k];
+    poff[k + 1] = poff[k] + (size_t)ps[k];
+  }
+  std::vector<double> host(off[count]);
+  for (int k = 0; k < count; ++k) {
+    const qsb_table* t = tables[k];
+    const int p = ps[k];
+    const double* g = gammas + poff[k];
+    const double* b = betas + poff[k];
+    double* rxcs = host.data() + off[k];
+    double* ang = rxcs + 4 * p;
+    double* lut = ang + 2 * p;
+    for (int i = 0; i < p; ++i) {
+      const double tf = -2.0 * b[i], ti = 2.0 * b[i];
+      rxcs[2 * i] = cos(tf / 2.0);
+      rxcs[2 * i + 1] = sin(tf / 2.0);
+      rxcs[2 * (p + i)] = cos(ti / 2.0);
+      rxcs[2 * (p + i) + 1] = sin(ti / 2.0);
+      ang[i] = -g[i];
+      ang[p + i] = g[i];
+    }
+    if (t->kind != 0)
+      for (int L = 0; L < 2 * p; ++L)
+        for (int v = 0; v < t->nvals; ++v) {
+          const double an = ang[L] * (t->vmin + (double)v);  // same product as prepare_luts
+          lut[2 * ((size_t)L * t->nvals + v)] = cos(an);
+          lut[2 * ((size_t)L * t->nvals + v) + 1] = sin(an);
+        }
+  }
+  // device: [staging][outputs][args]
+  const size_t stage_b = host.size() * sizeof(double), out_b = ooff[count] * sizeof(double);
+  const size_t args_b = (size_t)count * sizeof(SmallArgs);
+  QSB_TRY(ensure_small(ctx, stage_b + out_b + args_b + 256));
+  double* d_stage = (double*)ctx->d_small;
+  double* d_out = d_stage + host.size();
+  SmallArgs* d_args = (SmallArgs*)(((uintptr_t)(d_out + ooff[count]) + 15) & ~(uintptr_t)15);
+  std::vector<SmallArgs> args(count);
+  for (int k = 0; k < count; ++k) {
+    const qsb_table* t = tables[k];
+    SmallArgs& a = args[k];
+    a.ket = (double2*)kets[k];
+    a.table = t->values;
+    a.cidx = t->cidx;
+    a.rxcs = d_stage + off[k];
+    a.ang = a.rxcs + 4 * ps[k];
+    a.lut = (const double2*)(a.ang + 2 * ps[k]);
+    a.out = d_out + ooff[k];
+    a.plus_amp = 1.0 / sqrt((double)(1ull << t->n));
+    a.n = t->n;
+    a.p = ps[k];
+    a.kind = t->kind;
+    a.nvals = t->nvals;
+    a.mode = mode;
+    a.want_value = mode >= 1;
+  }
+  QSB_CUDA(cudaMemcpyAsync(d_stage, host.data(), stage_b, cudaMemcpyHostToDevice, ctx->stream));
+  QSB_CUDA(cudaMemcpyAsync(d_args, args.data(), args_b, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h2d_bytes += stage_b + args_b;
+  static bool attr = false;
+  if (!attr) {
+    QSB_CUDA(cudaFuncSetAttribute(k_small_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmem));
+    attr = true;
+  }
+  k_small_batch<<<count, kST, kSmallSmem, ctx->stream>>>(d_args);
+  QSB_CHECK_LAUNCH(ctx, "small-register batch");
+  QSB_CUDA(cudaMemcpyAsync(out, d_out, out_b, cudaMemcpyDeviceToHost, ctx->stream));
+  QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->d2h_bytes += out_b;
+  return QSB_OK;
+}
+
+}  // extern "C"

@@ -98,3 +98,25 @@ def test_concurrent_handles_from_threads():
     with ThreadPoolExecutor(max_workers=6) as pool:
         par = list(pool.map(run, cases))
     assert par == seq
+
+
+def test_batched_small_registers_equal_one_by_one():
+    """batch.value_and_grad_batch: one CTA per instance in one launch (the paper's
+    many-small-graphs regime) -- bit-identical to the per-handle calls"""
+    from paper_2407_13012_b200 import batch
+
+    suite = qs.generate_suite(vertex_range=(4, 11), instances=3, seed=7)
+    handles, params = [], []
+    rs = np.random.default_rng(1)
+    for k, (_, graph) in enumerate(suite[:24]):  # (name, Graph) pairs, n = 4..11
+        h = qs.create_handle(qs.maxcut_polynomial(graph), backend_name="b200")
+        p = 1 + k % 4
+        handles.append(h)
+        params.append(qs.QaoaParams(list(rs.uniform(-1, 1, p)), list(rs.uniform(-1, 1, p))))
+    got = batch.value_and_grad_batch(handles, params)
+    eb = batch.expectation_batch(handles, params)
+    for h, prm, (v, g), e in zip(handles, params, got, eb):
+        v1, g1 = qs.value_and_grad(h, prm)
+        assert v == v1 and e == v1
+        assert g.d_gammas == g1.d_gammas and g.d_betas == g1.d_betas
+        h.close()
