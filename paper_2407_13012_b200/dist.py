@@ -312,9 +312,25 @@ class TorchExchanger:
         return "cpu" if self.cpu else f"cuda:{self.device}"
 
     def setup(self, handle) -> None:
-        """P2P mode: export this shard's live/spare buffers, open every peer's."""
+        """P2P mode: export this shard's live/spare buffers, open every peer's.  If any
+        rank cannot (no peer access), every rank falls back to the NCCL all-to-all."""
         if not self.fused:
             return
+        import torch
+
+        ok = 1
+        try:
+            self._setup_p2p(handle)
+        except Exception:  # noqa: BLE001 -- decided collectively below
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=self._tdev())
+        self.dist.all_reduce(flag, op=self.dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            self.close()
+            self._peers, self._parity = {}, {}
+            self.fused = False
+
+    def _setup_p2p(self, handle) -> None:
         import torch
 
         self._ctx = handle.ctx.device.handle
@@ -354,7 +370,10 @@ class TorchExchanger:
 
     def close(self) -> None:
         for p_ in self._opened:
-            call("qsb_ipc_close", self._ctx, p_)
+            try:
+                call("qsb_ipc_close", self._ctx, p_)
+            except Exception:  # noqa: BLE001 -- best effort at teardown
+                pass
         self._opened = []
 
     def combine(self, per_rank_sums: list[np.ndarray]) -> np.ndarray:
