@@ -312,6 +312,15 @@ struct Runner {
   double plus_amp = 0.0;        // 0: 1/sqrt(2^n)
   unsigned maxgrid = 0;
   const qsb_shard_visit* swap = nullptr;  // fused qubit-swap store (sharded walk)
+  // Deferred gate scaling (window chain): the factored gates leave a real scale sigma^g
+  // on every amplitude; instead of multiplying it out at the end of every sweep, the
+  // chain carries it as `pend` (the vectors entering the next sweep are true/pend) and
+  // folds it into the reduction weights; it is applied only where a state becomes
+  // visible (the last sweep of a forward chain) or when it drifts towards the
+  // exponent range's ends.  (bra and ket always carry the same pending scale.)
+  bool defer = false;
+  double pend = 1.0;
+  bool apply_now = false;  // set by the chain for the sweep that must store true values
 
   int init(int total_sweeps_upper) {
     shapes = plan_sweeps(n);
@@ -387,27 +396,40 @@ struct Runner {
     a.gb = g1.gb;
     a.plus_amp = plus_amp > 0.0 ? plus_amp : 1.0 / sqrt((double)(1ull << n));
     const double s1 = g1.sigma * g1.sigma;
+    // pending scale of the input vectors (deferred scaling; 1 otherwise) and its square,
+    // the weight of every bra/ket or ket/ket contraction taken on raw values
+    const double S = (defer && !exact) ? pend : 1.0, S2 = S * S;
     // xsum weights: the pending gate scale^2 where the kernel takes the xsum (fast: after
     // the phase's gates; exact: sigma = 1)
     auto after = [](const int* gb, const uint8_t* ap, int p) { return gb[p] + __builtin_popcount(ap[p]); };
     uint8_t ap1[kMaxPhases];
     for (int p = 0; p < kMaxPhases; ++p) ap1[p] = a.ph[p].apply;
-    for (int p = 0; p < a.nphase; ++p) a.xs_w[p] = ipow(s1, exact ? gbp[p] : after(gbp, ap1, p));
+    for (int p = 0; p < a.nphase; ++p) a.xs_w[p] = S2 * ipow(s1, exact ? gbp[p] : after(gbp, ap1, p));
+    double G;  // this sweep's gate scale
     a.w0 = a.w1 = 1.0;
     if (mode != SM_PLAIN) {
       // pass-1 scale is still pending at the mid ops and throughout pass 2
       const double m = ipow(s1, gates);
-      a.w0 = a.w1 = m;
+      a.w0 = a.w1 = S2 * m;
       a.form2 = g2.form;
       a.ga2 = g2.ga;
       a.gb2 = g2.gb;
-      for (int p = 0; p < a.nphase; ++p) a.xs_w2[p] = m * ipow(g2.sigma * g2.sigma, after(gbp2, a.apply2, p));
-      a.post_scale = ipow(g1.sigma, gates) * ipow(g2.sigma, gates2);
-      if (gates + gates2 > 0) flags |= SF_POST_SCALE;
+      for (int p = 0; p < a.nphase; ++p) a.xs_w2[p] = S2 * m * ipow(g2.sigma * g2.sigma, after(gbp2, a.apply2, p));
+      G = ipow(g1.sigma, gates) * ipow(g2.sigma, gates2);
     } else {
       a.form2 = g1.form;
-      a.post_scale = ipow(g1.sigma, gates);
-      if (!exact && gates > 0) flags |= SF_POST_SCALE;
+      G = exact ? 1.0 : ipow(g1.sigma, gates);
+      a.w1 = S2;  // pre-op <bra|C|ket> on the raw input
+    }
+    // apply the scale (true values stored) or carry it to the next sweep
+    const double out_scale = S * G;
+    const bool carry = defer && !exact && !apply_now && fabs(out_scale) > 1e-150 && fabs(out_scale) < 1e150;
+    if (carry) {
+      a.post_scale = 1.0;
+      if (mode == SM_PLAIN) a.w0 = out_scale * out_scale;  // post ops on raw values
+    } else {
+      a.post_scale = out_scale;
+      if (!exact && out_scale != 1.0) flags |= SF_POST_SCALE;
     }
     a.flags = flags;
     if (swap && swap->swap_g) {
@@ -431,6 +453,7 @@ struct Runner {
     }
     grids.push_back(grid);
     if (idx_out) *idx_out = idx;
+    if (defer && !exact) pend = carry ? out_scale : 1.0;
     return QSB_OK;
   }
 
@@ -542,6 +565,11 @@ int run_chain(Runner& R, double2* ket, double2* bra, int p, const double* gammas
   const std::vector<Visit> vis = chain_visits(n, wins, p, fwd, bwd);
   const int M = (int)vis.size();
   const bool merge = merge_enabled() && wins.size() >= 2;
+  {
+    const char* e = getenv("QSB_NO_DEFER");  // A/B: multiply the gate scale out in every sweep
+    R.defer = !(e && atoi(e));
+    R.pend = 1.0;
+  }
   const double2 one = make_double2(1.0, 0.0);
   const uint64_t nvals = R.t->kind != 0 ? (uint64_t)R.t->nvals : 0;
   auto fwd_lut = [&](int i) { return R.t->kind != 0 ? R.t->d_lut + (size_t)i * nvals : nullptr; };
@@ -588,6 +616,7 @@ int run_chain(Runner& R, double2* ket, double2* bra, int p, const double* gammas
         lut = inv_lut(v.layer);
         ang = gammas[v.layer];
       }
+      R.apply_now = !bwd && u + 2 >= M;  // a forward chain stores true values at its end
       QSB_TRY(R.sweep_any(nv, mode, win_of(v), pass2, ket, bra, gate_of(v), gate_of(w), f, lut, ang, one, true, &idx));
       if (kind == 2 && want_value) contribs.push_back({idx, 0, 0, 0});
       if (v.bwd) contribs.push_back({idx, 2, 2, v.layer});
@@ -633,6 +662,7 @@ int run_chain(Runner& R, double2* ket, double2* bra, int p, const double* gammas
     if (post_expect) f |= SF_POST_EXPECT;
     if (post_dinner) f |= SF_POST_DINNER | SF_NO_STORE;
     if (v.bwd) f |= SF_XSUM;
+    R.apply_now = !bwd && u == M - 1;
     QSB_TRY(R.sweep(v.bwd ? 2 : 1, win_of(v), ket, bra, gate_of(v), f, lut, ang, one, true, &idx));
     if (post_expect) contribs.push_back({idx, 0, 0, 0});
     if (post_dinner) contribs.push_back({idx, 0, 1, v.layer});

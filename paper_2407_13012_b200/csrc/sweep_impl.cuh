@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     // ---------------------------------------------------------------- post
     // the map the tile ends in: the last phase (plain) or the first (merged)
     constexpr int RL = shape_phase(SH, MODE == SM_PLAIN ? NP - 1 : 0).reg_l;
-    if constexpr (!EXACT) {  // factored gates: one real scale per sweep (1.0 if no gates)
+    if (!EXACT && (flags & SF_POST_SCALE)) {  // factored gates: one real scale per sweep (unless deferred)
       const double sc = a.post_scale;
 #pragma unroll
       for (int q = 0; q < NV; ++q)
