@@ -264,6 +264,16 @@ def load_peaks() -> dict:
     return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
+def survey_model(n: int, p: int, ms_step: float, peak_gbs: float) -> dict:
+    N = float(1 << n)
+    S = 1 + -(-(n - 12) // 9) if n > 12 else 1  # A window + 9-qubit B windows
+    model = (p * (96 * S + 16) - 16) * N
+    t100 = model / (peak_gbs * 1e9) * 1e3
+    return {"model_bytes": model, "sweeps_per_layer": S, "effective_gbs": model / (ms_step * 1e-3) / 1e9,
+            "effective_frac": model / (ms_step * 1e-3) / 1e9 / peak_gbs, "model_ms_at_peak": t100,
+            "north_star_ms_at_70pct": t100 / 0.7}
+
+
 def kernel_label(kind: str) -> str:
     """sweep kind (DeviceContext.prof_kind_name) -> the k_sweep instantiation it runs"""
     vec, *mode, win = kind.split("_")
@@ -528,6 +538,11 @@ def run_b200(args, rank: int, world: int, dist) -> None:
         },
         "sweeps_share_of_step": total_sweep_ms / ms,
         "step_hbm_gbs": all_bytes / (ms * 1e-3) / 1e9,
+        # SURVEY.md §8(d)'s byte model for value_and_grad (S = 3 sweeps per layer, one
+        # pass per window per layer): [p(96S+16) - 16] N.  The window chain moves fewer
+        # bytes (above); against the model's bytes the step runs at this effective rate,
+        # and the north star's ">= 70% of HBM roofline" is <= t_model / 0.7.
+        "vs_survey_model": survey_model(args.n, args.p, ms / args.steps, peaks["hbm_gbs"]),
         "e2e": {
             "value": world * args.steps / (wall_ms / 1e3),
             "unit": UNIT,
