@@ -872,8 +872,15 @@ static int value_and_grad_perop(qsb_ctx* ctx, qsb_table* t, double2* ket, double
     double xs[2], di[2];
     QSB_TRY(xsum_exact(ctx, bra, ket, len, n, xs));
     db[i] = -2.0 * xs[1];
-    QSB_TRY(rx_layer_perop(ctx, bra, n, 2.0 * betas[i]));
-    QSB_TRY(rx_layer_perop(ctx, ket, n, 2.0 * betas[i]));
+    // Rx(+2 beta) layers: the exact fused sweeps (FMA-free, ascending qubit order:
+    // bit-identical to n rx_qubit passes) for n >= 12, else the per-qubit kernel
+    if (n >= kSweepT) {
+      QSB_TRY(qsb_rx_layer(ctx, (double*)bra, n, 2.0 * betas[i], QSB_EXACT));
+      QSB_TRY(qsb_rx_layer(ctx, (double*)ket, n, 2.0 * betas[i], QSB_EXACT));
+    } else {
+      QSB_TRY(rx_layer_perop(ctx, bra, n, 2.0 * betas[i]));
+      QSB_TRY(rx_layer_perop(ctx, ket, n, 2.0 * betas[i]));
+    }
     QSB_TRY(diag_inner_exact(ctx, bra, t->values, ket, len, di));
     dg[i] = 2.0 * di[1];
     QSB_TRY(qsb_table_phase(ctx, t, (double*)bra, -gammas[i]));
