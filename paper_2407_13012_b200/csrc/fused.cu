@@ -344,7 +344,7 @@ struct Runner {
       if (!(flags & SF_NO_STORE)) b += 16.0 * N;
     } else {
       b += (mode == SM_BRIDGE || (flags & SF_BRA_FROM_KET)) ? 16.0 * N : 32.0 * N;
-      if (!(flags & SF_NO_STORE)) b += 32.0 * N;
+      if (!(flags & SF_NO_STORE)) b += (flags & SF_KEEP_V0) ? 16.0 * N : 32.0 * N;
     }
     if ((flags & kTableOps) || mode == SM_BRIDGE) b += tb * N;
     return b;
@@ -611,12 +611,16 @@ int run_chain(Runner& R, double2* ket, double2* bra, int p, const double* gammas
         nv = 2;
         if (want_value) f |= SF_MID_EXPECT;
         f |= SF_XSUM2;
+        // the ket leaves the bridge as it came in (Rx(+2b) Rx(-2b) = 1): keep HBM's copy
+        // instead of storing it -- when that copy carries no pending scale; the bra is then
+        // stored with its scale applied so both vectors are true values afterwards
+        if (R.pend == 1.0) f |= SF_KEEP_V0;
       } else {  // backward layer i -> i-1: <bra|C|ket>, then the inverse phase exp(+i g_i C)
         f |= SF_XSUM | SF_MID_DINNER | SF_MID_PHASE | SF_XSUM2;
         lut = inv_lut(v.layer);
         ang = gammas[v.layer];
       }
-      R.apply_now = !bwd && u + 2 >= M;  // a forward chain stores true values at its end
+      R.apply_now = (!bwd && u + 2 >= M) || (f & SF_KEEP_V0);  // true values where the chain needs them
       QSB_TRY(R.sweep_any(nv, mode, win_of(v), pass2, ket, bra, gate_of(v), gate_of(w), f, lut, ang, one, true, &idx));
       if (kind == 2 && want_value) contribs.push_back({idx, 0, 0, 0});
       if (v.bwd) contribs.push_back({idx, 2, 2, v.layer});

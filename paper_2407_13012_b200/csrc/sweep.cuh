@@ -28,6 +28,8 @@ enum SweepFlags : uint32_t {
   SF_MID_DINNER = 1u << 10,  // NV=2 merged: slot1 += T*Im(conj(bra) ket) between the passes
   SF_MID_EXPECT = 1u << 11,  // bridge: slot0 += T*|ket|^2 between the passes
   SF_XSUM2 = 1u << 12,       // NV=2: slot3 += xsum over the second pass's qubits
+  SF_KEEP_V0 = 1u << 13,     // bridge: v0 is not stored -- pass 2 undoes pass 1 on the ket
+                             // (Rx(+2b) Rx(-2b) = 1), so HBM already holds its result
 };
 
 // A merged sweep applies two layers' gates to one window per HBM pass.  The chain

@@ -586,6 +586,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
       }
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
+        if (q == 0 && MODE == SM_BRIDGE && (flags & SF_KEEP_V0)) continue;
         double2* dst = out[q] + g1;
 #pragma unroll
         for (int j = 0; j < NR; ++j) st_stream(dst + gofs<IS_A>((uint32_t)j << RL, glo), v[q][j]);
@@ -712,7 +713,7 @@ template <int NV, int MODE, int F1, int SA = SH_A2, int SB = SH_B2, int GR = 1>
 int launch_merged_f1(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
   auto L = [&](auto k) { return decltype(k)::launch(ctx, a, g); };
   // every flag a merged / bridge sweep of this kind can carry (run_chain, fused.cu)
-  constexpr uint32_t M = SF_POST_SCALE | (MODE == SM_BRIDGE ? (uint32_t)(SF_MID_EXPECT | SF_XSUM2)
+  constexpr uint32_t M = SF_POST_SCALE | (MODE == SM_BRIDGE ? (uint32_t)(SF_MID_EXPECT | SF_XSUM2 | SF_KEEP_V0)
                                           : NV == 1 ? (uint32_t)SF_MID_PHASE
                                                     : (uint32_t)(SF_XSUM | SF_MID_DINNER | SF_MID_PHASE | SF_XSUM2));
   if ((a.flags & ~M) != 0) return invalid("internal: unexpected flags 0x%x for a merged sweep", a.flags);
