@@ -234,11 +234,8 @@ int small_run(qsb_ctx* ctx, qsb_table* t, double2* ket, int p, const double* gam
   a.mode = mode;
   a.want_value = value != nullptr;
   const size_t smem = kSmallSmem;
-  static bool attr = false;
-  if (!attr) {
-    QSB_CUDA(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  static const cudaError_t attr = cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  QSB_CUDA(attr);
   k_small<<<1, kST, smem, ctx->stream>>>(a);
   QSB_CHECK_LAUNCH(ctx, "small-register circuit");
   if (value || mode >= 2) {
@@ -335,11 +332,9 @@ int qsb_small_batch(qsb_ctx* ctx, int count, qsb_table* const* tables, double* c
   QSB_CUDA(cudaMemcpyAsync(d_stage, host.data(), stage_b, cudaMemcpyHostToDevice, ctx->stream));
   QSB_CUDA(cudaMemcpyAsync(d_args, args.data(), args_b, cudaMemcpyHostToDevice, ctx->stream));
   ctx->h2d_bytes += stage_b + args_b;
-  static bool attr = false;
-  if (!attr) {
-    QSB_CUDA(cudaFuncSetAttribute(k_small_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmem));
-    attr = true;
-  }
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(k_small_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmem);
+  QSB_CUDA(attr);
   k_small_batch<<<count, kST, kSmallSmem, ctx->stream>>>(d_args);
   QSB_CHECK_LAUNCH(ctx, "small-register batch");
   QSB_CUDA(cudaMemcpyAsync(out, d_out, out_b, cudaMemcpyDeviceToHost, ctx->stream));

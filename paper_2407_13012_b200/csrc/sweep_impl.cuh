@@ -636,15 +636,24 @@ template <int SH, int NV, int FORM, bool KSIN, bool FULL, int MODE = SM_PLAIN, i
 struct SweepKernel {
   static constexpr int threads = GR * (32 << shape_w(SH));
   static int grid(qsb_ctx* ctx, uint64_t ntiles, unsigned* g) {
-    static int occ = -1;  // per process; one device type
-    if (occ < 0) {
-      QSB_CUDA(cudaFuncSetAttribute(k_sweep<SH, NV, FORM, KSIN, FULL, MODE, FORM2, GR, FM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)kSmemBytes));
+    // once per process (thread-safe static initialisation; one device type)
+    struct Init {
+      cudaError_t err;
+      int occ;
+    };
+    static const Init init = [] {
+      Init r{cudaFuncSetAttribute(k_sweep<SH, NV, FORM, KSIN, FULL, MODE, FORM2, GR, FM>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes),
+             1};
       int o = 0;
-      QSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sweep<SH, NV, FORM, KSIN, FULL, MODE, FORM2, GR, FM>, threads, kSmemBytes));
-      occ = o < 1 ? 1 : o;
-    }
-    const uint64_t want = (uint64_t)ctx->num_sms * occ;
+      if (r.err == cudaSuccess)
+        r.err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sweep<SH, NV, FORM, KSIN, FULL, MODE, FORM2, GR, FM>,
+                                                              threads, kSmemBytes);
+      r.occ = o < 1 ? 1 : o;
+      return r;
+    }();
+    QSB_CUDA(init.err);
+    const uint64_t want = (uint64_t)ctx->num_sms * init.occ;
     *g = (unsigned)(ntiles < want ? ntiles : want);
     return QSB_OK;
   }
