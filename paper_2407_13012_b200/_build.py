@@ -52,16 +52,19 @@ def _needs_rebuild() -> bool:
     return any(p.stat().st_mtime > lib_m for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _needs_rebuild():
+def build(force: bool = False, verbose: bool = False, defines: tuple[str, ...] = (), lib: Path = LIB,
+          objdir: Path = BUILD) -> Path:
+    """defines / lib / objdir: experiment builds (tools/build_variant.py), e.g.
+    defines=("QSB_EXCH_PRESYNC=1",) into a second library selected with QSB_LIB."""
+    if lib == LIB and not force and not _needs_rebuild():
         return LIB
-    BUILD.mkdir(parents=True, exist_ok=True)
+    objdir.mkdir(parents=True, exist_ok=True)
     cc = nvcc()
     srcs = _sources()
 
     def compile_one(src: Path) -> tuple[Path, str]:
-        obj = BUILD / (src.stem + ".o")
-        cmd = [cc, *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        obj = objdir / (src.stem + ".o")
+        cmd = [cc, *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", str(src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src.name}:\n{res.stderr}")
@@ -70,16 +73,16 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     with ThreadPoolExecutor(max_workers=min(8, len(srcs))) as pool:
         results = list(pool.map(compile_one, srcs))
     log = "".join(f"== {o.name}\n{e}" for o, e in results)
-    (BUILD / "ptxas.log").write_text(log)
+    (objdir / "ptxas.log").write_text(log)
     if verbose:
         sys.stderr.write(log)
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [cc, *ARCH, "-shared", "-o", str(tmp), *[str(o) for o, _ in results], "-cudart", "static"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -10,6 +10,7 @@ raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
@@ -17,7 +18,8 @@ import numpy as np
 
 from .errors import ContractViolation, ResourceError
 
-_LIB_PATH = Path(__file__).resolve().parent / "libqsb.so"
+# QSB_LIB: an experiment build of the same library (tools/build_variant.py)
+_LIB_PATH = Path(os.environ["QSB_LIB"]) if os.environ.get("QSB_LIB") else Path(__file__).resolve().parent / "libqsb.so"
 
 QSB_OK, QSB_EINVAL, QSB_ENOMEM, QSB_ECUDA, QSB_ENODEV = 0, 1, 2, 3, 4
 QSB_EXACT = 1

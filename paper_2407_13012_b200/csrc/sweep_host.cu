@@ -1,4 +1,5 @@
 // Host side of the fused sweep: kernel dispatch and TMA descriptor encoding.
+#include <stdlib.h>
 #include <string.h>
 
 #include "sweep.cuh"
@@ -24,6 +25,14 @@ int launch_sweep_m_nv2_s(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_bridge(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_m_nv2_r3_c(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_m_nv2_r3_s(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int launch_sweep_m_nv2_t_c(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int launch_sweep_m_nv2_t_s(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+
+// merged bra/ket sweeps: staggered schedule (default; QSB_STAG=0: lock-step)
+static bool stag_enabled() {
+  const char* e = getenv("QSB_STAG");
+  return e ? atoi(e) != 0 : true;
+}
 
 int launch_sweep(qsb_ctx* ctx, int nv, bool exact, SweepArgs& a, unsigned* gout) {
   if (a.mode != SM_PLAIN) {
@@ -39,6 +48,7 @@ int launch_sweep(qsb_ctx* ctx, int nv, bool exact, SweepArgs& a, unsigned* gout)
       return c ? launch_sweep_m_nv1_r4_c(ctx, a, gout) : launch_sweep_m_nv1_r4_s(ctx, a, gout);
     }
     if (r == 3) return c ? launch_sweep_m_nv2_r3_c(ctx, a, gout) : launch_sweep_m_nv2_r3_s(ctx, a, gout);
+    if (stag_enabled()) return c ? launch_sweep_m_nv2_t_c(ctx, a, gout) : launch_sweep_m_nv2_t_s(ctx, a, gout);
     return c ? launch_sweep_m_nv2_c(ctx, a, gout) : launch_sweep_m_nv2_s(ctx, a, gout);
   }
   if (exact || a.form == GF_EXACT) return nv == 1 ? launch_sweep_exact_nv1(ctx, a, gout) : launch_sweep_exact_nv2(ctx, a, gout);

@@ -28,6 +28,7 @@
 // phase's gates) and <psi|C|psi>.
 #pragma once
 #include <type_traits>
+#include <utility>
 
 #include "sweep.cuh"
 
@@ -167,6 +168,49 @@ __device__ __forceinline__ void gate_bits(double2 (&v)[NV][NR], uint32_t apply, 
   }
 }
 
+// gates on the register bits in `apply`, one vector
+template <int FORM, int NR, int R>
+__device__ __forceinline__ void gate_vec(double2 (&u)[NR], uint32_t apply, double ga, double gb) {
+#pragma unroll
+  for (int b = 0; b < R; ++b) {
+    if (apply & (1u << b)) {
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        if (j & (1 << b)) continue;
+        butterfly<FORM>(u[j], u[j | (1 << b)], ga, gb);
+      }
+    }
+  }
+}
+
+template <class F, int... I>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, I...>) {
+  (f(std::integral_constant<int, I>{}), ...);
+}
+// f(integral_constant<int, 0>) ... f(integral_constant<int, N-1>), in order
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
+
+// an exchange between phases p and q of shape sh keeps every amplitude in its warp
+template <int W>
+__host__ __device__ constexpr bool stag_local(int sh, int p, int q) {
+  bool l = true;
+  for (int b = 0; b < W; ++b) l = l && shape_phase(sh, p).warps[b] == shape_phase(sh, q).warps[b];
+  return l;
+}
+
+// compile-time marker in a kernel's flag mask FM: run a merged bra/ket sweep with the
+// staggered schedule (see the kernel); never set in SweepArgs::flags
+constexpr uint32_t kStagBit = 1u << 30;
+#ifndef QSB_STAG_EARLY_STORE
+#define QSB_STAG_EARLY_STORE 1  // staggered sweeps store the lead during the lag's last stage
+#endif
+#ifndef QSB_EXCH_PRESYNC
+#define QSB_EXCH_PRESYNC 0  // 1: a CTA barrier before every warp-crossing exchange (A/B builds)
+#endif
+
 // Im sum_{b in apply} <bra|X_b|ket> over this thread's register pairs (NV == 2)
 template <int NR, int R>
 __device__ __forceinline__ double xsum_bits(const double2 (&v)[2][NR], uint32_t apply) {
@@ -210,6 +254,9 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
   static_assert(MODE == SM_PLAIN || !EXACT, "merged sweeps are fast-mode only");
   static_assert(MODE != SM_BRIDGE || NV == 2, "a bridge sweep produces the bra");
   static_assert(GR == 1 || (GR == 2 && NV == 1), "warp groups: single-vector sweeps only");
+  // staggered merged bra/ket sweep: the two vectors run half a stage apart, so one
+  // vector's shared-memory exchange is in flight while the other's gates run
+  constexpr bool STAG = NV == 2 && MODE == SM_MERGED && GR == 1 && FM != 0xffffffffu && (FM & kStagBit) != 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(smem_raw);
   const uint32_t cring_s = ring_s + kRing * kSlotBytes;
@@ -228,6 +275,10 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int s = 0; s < GR * kRing; ++s) mbar_init(bar_s + 8 * s, 1);
+    if constexpr (STAG) {  // exchange barriers of the two vectors: one arrival per warp
+      mbar_init(bar_s + 8 * 6, 1u << W);
+      mbar_init(bar_s + 8 * 7, 1u << W);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (!KSIN && a.kind == 1 && (flags & (SF_PRE_PHASE | SF_MID_PHASE))) {  // u8 LUT in smem
@@ -297,6 +348,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
   auto wait_seq = [&](uint64_t s) { mbar_wait(seq_bar(s), (uint32_t)((s / (GR * kRing)) & 1)); };
 
   double acc0 = 0.0, acc0b = 0.0, acc1 = 0.0, acc1b = 0.0, acc2 = 0.0, acc3 = 0.0;
+  uint32_t fph[2] = {0u, 0u};  // STAG: phase parity of the two exchange barriers
   double2 v[NV][NR];
 
   // NV=1: tile k lands in slot k % 3, two tiles in flight.  NV=2: bra / ket of tile k
@@ -349,10 +401,12 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
 #pragma unroll
         for (int j = 0; j < NR; ++j) v[1][j] = lds(pb + (((uint32_t)j << P0.reg_l) * 16u));
       }
-      wait_seq(2 * k + 1);
-      const uint32_t p0 = xs_addr + lb * 16u;
+      if constexpr (!STAG) {  // staggered: the ket lands in stage 0
+        wait_seq(2 * k + 1);
+        const uint32_t p0 = xs_addr + lb * 16u;
 #pragma unroll
-      for (int j = 0; j < NR; ++j) v[0][j] = lds(p0 + (((uint32_t)j << P0.reg_l) * 16u));
+        for (int j = 0; j < NR; ++j) v[0][j] = lds(p0 + (((uint32_t)j << P0.reg_l) * 16u));
+      }
     }
 
     // ---------------------------------------------------------------- table views
@@ -449,7 +503,11 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
       for (int b = 0; b < W; ++b) local = local && Q.warps[b] == P.warps[b];
       const uint32_t nlb = lbase<W>(P, lane, warp);
       const uint32_t so = swz(lb) * 16u, sn = swz(nlb) * 16u;
-      if (local) __syncwarp(); else gsync();
+      // no CTA barrier before the stores: each thread overwrites only the slots it read
+      // under map Q (the landing read in the natural layout stays within the warp)
+      // (kept for plain bra/ket B sweeps, where it measured faster: warps in step)
+      constexpr bool PRESYNC = QSB_EXCH_PRESYNC || (NV == 2 && MODE == SM_PLAIN && !IS_A);
+      if (PRESYNC && !local) gsync(); else __syncwarp();
 #pragma unroll
       for (int q = 0; q < decltype(nvx)::value; ++q) {
         const uint32_t xa = q == 0 ? xs_addr : xb_addr;
@@ -485,7 +543,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
 
     // ---------------------------------------------------------------- pass 1
 #pragma unroll
-    for (int p = 0; p < NP; ++p) {
+    for (int p = 0; p < (STAG ? 0 : NP); ++p) {
       if (p > 0) exchange(shape_phase(SH, p - 1), shape_phase(SH, p), std::integral_constant<int, NVA>{});
       if (MODE == SM_PLAIN && p == NP - 1) release();
       // FULL: compile-time gate mask (no branches around the register tile)
@@ -501,13 +559,15 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     }
 
     // ---------------------------------------------------------------- mid ops + pass 2
-    if constexpr (MODE != SM_PLAIN) {
+    // mid ops: the diagonal work between the passes, both vectors in the last map
+    // (local base lbm)
+    auto mid_ops = [&](uint32_t lbm) {
       constexpr int RM = shape_phase(SH, NP - 1).reg_l;
       with_table([&](auto tv) {
-        const uint64_t g1 = base + gofs<IS_A>(lb, glo);
+        const uint64_t g1 = base + gofs<IS_A>(lbm, glo);
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
-          const uint32_t l = lb | ((uint32_t)j << RM);
+          const uint32_t l = lbm | ((uint32_t)j << RM);
           const uint64_t g = g1 + gofs<IS_A>((uint32_t)j << RM, glo);
           if constexpr (MODE == SM_BRIDGE) {
             const double t = tv.val(l, g);
@@ -534,6 +594,9 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
           }
         }
       });
+    };
+    if constexpr (MODE != SM_PLAIN && !STAG) {
+      mid_ops(lb);
 #pragma unroll
       for (int pp = 0; pp < NP; ++pp) {
         const int p = NP - 1 - pp;
@@ -545,15 +608,126 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
       }
     }
 
-    // ---------------------------------------------------------------- post
+    // ---------------------------------------------------------------- post helpers
     // the map the tile ends in: the last phase (plain) or the first (merged)
     constexpr int RL = shape_phase(SH, MODE == SM_PLAIN ? NP - 1 : 0).reg_l;
-    if (!EXACT && (flags & SF_POST_SCALE)) {  // factored gates: one real scale per sweep (unless deferred)
+    // factored gates: one real scale per sweep (unless deferred)
+    auto scale_vec = [&](int q) {
       const double sc = a.post_scale;
 #pragma unroll
-      for (int q = 0; q < NV; ++q)
+      for (int j = 0; j < NR; ++j) v[q][j] = make_double2(v[q][j].x * sc, v[q][j].y * sc);
+    };
+    auto store_vec = [&](int q) {
+      uint64_t g1 = base + gofs<IS_A>(lb, glo);
+      double2* dst = q == 0 ? a.v0 : a.v1;
+      if (a.sw_g) {  // qubit swap fused into the store: the whole tile goes to shard c
+        const int hb = a.sw_nl - a.sw_g;
+        const uint64_t c = base >> hb;
+        dst = a.sw_out[q][c];
+        g1 = (g1 & ((1ull << hb) - 1ull)) | ((uint64_t)a.sw_rank << hb);
+      }
+      dst += g1;
 #pragma unroll
-        for (int j = 0; j < NR; ++j) v[q][j] = make_double2(v[q][j].x * sc, v[q][j].y * sc);
+      for (int j = 0; j < NR; ++j) st_stream(dst + gofs<IS_A>((uint32_t)j << RL, glo), v[q][j]);
+    };
+
+    // ------------------------------------------- staggered merged bra/ket sweep
+    // Stages s = 0 .. 2NP-1 visit the maps P0 .. P(NP-1), P(NP-1) .. P0 (pass 1 gates,
+    // mid ops after stage NP-1, pass 2 gates).  The lead vector (the bra: it lands
+    // first) runs half a stage ahead of the lag (the ket): in every stage the lead is
+    // gated while the lag's load from shared memory is in flight, and the lag is gated
+    // while the lead's exchange is.  An exchange needs no barrier before its stores
+    // (each thread writes the slots it alone read, under the map it leaves; the landing
+    // read is per-warp, hence the __syncwarp) and one per-vector mbarrier (an arrival
+    // per warp) before its loads when it moves warp bits -- no CTA-wide barrier until
+    // the slots are released for the next tile.
+    if constexpr (STAG) {
+      using QLc = std::integral_constant<int, 1>;  // lead (bra)
+      using QGc = std::integral_constant<int, 0>;  // lag (ket)
+      auto xstore = [&](auto qc, const PhaseSpec Q, auto localc) {
+        constexpr int q = decltype(qc)::value;
+        const uint32_t xa = q == 0 ? xs_addr : xb_addr;
+        const uint32_t so = swz(lbase<W>(Q, lane, warp)) * 16u;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < NR; ++j) sts(xa + (so ^ (swz((uint32_t)j << Q.reg_l) * 16u)), v[q][j]);
+        if constexpr (!decltype(localc)::value) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_s + 8u * (6u + (uint32_t)q));
+        }
+      };
+      auto xload = [&](auto qc, const PhaseSpec P, auto localc) {
+        constexpr int q = decltype(qc)::value;
+        const uint32_t xa = q == 0 ? xs_addr : xb_addr;
+        if constexpr (decltype(localc)::value) {
+          __syncwarp();
+        } else {
+          mbar_wait(bar_s + 8u * (6u + (uint32_t)q), fph[q]);
+          fph[q] ^= 1u;
+        }
+        const uint32_t sn = swz(lbase<W>(P, lane, warp)) * 16u;
+#pragma unroll
+        for (int j = 0; j < NR; ++j) v[q][j] = lds(xa + (sn ^ (swz((uint32_t)j << P.reg_l) * 16u)));
+      };
+      static_for<2 * NP>([&](auto sc) {
+        constexpr int s = decltype(sc)::value;
+        constexpr int p = s < NP ? s : 2 * NP - 1 - s;
+        constexpr PhaseSpec M = shape_phase(SH, p);
+        // an exchange follows this stage unless it ends pass 1 (same map) or the sweep
+        constexpr bool exch = s != NP - 1 && s != 2 * NP - 1;
+        constexpr int pn = s + 1 < NP ? s + 1 : 2 * NP - 2 - s;  // map of stage s+1
+        constexpr bool loc = exch && stag_local<W>(SH, p, pn);
+        const uint32_t apply = s < NP ? (FULL ? shape_apply(SH, p) : a.ph[p].apply)
+                                      : (FULL ? shape_apply_rev(SH, p) : a.apply2[p]);
+        auto gates = [&](auto qc) {
+          constexpr int q = decltype(qc)::value;
+          if constexpr (s < NP) gate_vec<FORM, NR, R>(v[q], apply, a.ga, a.gb);
+          else gate_vec<FORM2, NR, R>(v[q], apply, a.ga2, a.gb2);
+        };
+        gates(QLc{});
+        if constexpr (s == 0) {  // the lag lands (natural layout)
+          wait_seq(2 * k + 1);
+          const uint32_t p0 = xs_addr + lb * 16u;
+#pragma unroll
+          for (int j = 0; j < NR; ++j) v[0][j] = lds(p0 + (((uint32_t)j << M.reg_l) * 16u));
+        } else if constexpr (s != NP) {
+          constexpr int pp = s - 1 < NP ? s - 1 : 2 * NP - s;  // map of stage s-1
+          xload(QGc{}, M, std::integral_constant<bool, stag_local<W>(SH, pp, p)>{});
+        }
+        if constexpr (exch) xstore(QLc{}, M, std::integral_constant<bool, loc>{});
+        if constexpr (s == 2 * NP - 1) {
+          release();  // the lag's last read: refill both slots
+          // the lead is final: its stores drain while the lag is gated (scaled here, so
+          // its last xsum weight is divided by the scale)
+          if constexpr (QSB_STAG_EARLY_STORE) {
+            if (!EXACT && (flags & SF_POST_SCALE)) scale_vec(1);
+            if (!(flags & SF_NO_STORE)) store_vec(1);
+          }
+        }
+        gates(QGc{});
+        if constexpr (s < NP) {
+          if (flags & SF_XSUM) xsum(acc2, a.xs_w[p], apply);
+        } else {
+          double w = a.xs_w2[p];
+          if constexpr (s == 2 * NP - 1 && QSB_STAG_EARLY_STORE) {
+            if (!EXACT && (flags & SF_POST_SCALE)) w /= a.post_scale;
+          }
+          if (flags & SF_XSUM2) xsum(acc3, w, apply);
+        }
+        if constexpr (s == NP - 1) mid_ops(lbase<W>(M, lane, warp));
+        if constexpr (exch) {
+          xload(QLc{}, shape_phase(SH, pn), std::integral_constant<bool, loc>{});
+          xstore(QGc{}, M, std::integral_constant<bool, loc>{});
+        }
+      });
+    }
+
+    // ---------------------------------------------------------------- post
+    // (STAG: the lead is scaled and stored in the last stage)
+    constexpr int Q0 = 0, Q1 = STAG && QSB_STAG_EARLY_STORE ? 1 : NV;  // vectors scaled / stored here
+    if (!EXACT && (flags & SF_POST_SCALE)) {
+#pragma unroll
+      for (int q = Q0; q < Q1; ++q) scale_vec(q);
     }
     if constexpr (MODE == SM_PLAIN) {
       // post ops: <psi|C|psi> (NV=1) or <bra|C|ket> (NV=2) after the gates, in the last map
@@ -575,21 +749,10 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     // MEMBAR then does not wait for this tile's 64 KB of stores to drain.
     if constexpr (NV == 1) fence_proxy_async();
     if (!(flags & SF_NO_STORE)) {
-      uint64_t g1 = base + gofs<IS_A>(lb, glo);
-      double2* out[2] = {a.v0, a.v1};
-      if (a.sw_g) {  // qubit swap fused into the store: the whole tile goes to shard c
-        const int hb = a.sw_nl - a.sw_g;
-        const uint64_t c = base >> hb;
-        out[0] = a.sw_out[0][c];
-        out[1] = a.sw_out[1][c];
-        g1 = (g1 & ((1ull << hb) - 1ull)) | ((uint64_t)a.sw_rank << hb);
-      }
 #pragma unroll
-      for (int q = 0; q < NV; ++q) {
+      for (int q = Q0; q < Q1; ++q) {
         if (q == 0 && MODE == SM_BRIDGE && (flags & SF_KEEP_V0)) continue;
-        double2* dst = out[q] + g1;
-#pragma unroll
-        for (int j = 0; j < NR; ++j) st_stream(dst + gofs<IS_A>((uint32_t)j << RL, glo), v[q][j]);
+        store_vec(q);
       }
     }
     if constexpr (NV == 1) {
@@ -718,14 +881,16 @@ int launch_fast(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
 
 // merged / bridge instantiations (fast mode; shapes SA / SB of one register family).  Table ops between
 // the passes dispatch on the table kind at run time (KSIN = false).
-template <int NV, int MODE, int F1, int SA = SH_A2, int SB = SH_B2, int GR = 1>
+template <int NV, int MODE, int F1, int SA = SH_A2, int SB = SH_B2, int GR = 1, bool STG = false>
 int launch_merged_f1(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
   auto L = [&](auto k) { return decltype(k)::launch(ctx, a, g); };
   // every flag a merged / bridge sweep of this kind can carry (run_chain, fused.cu)
-  constexpr uint32_t M = SF_POST_SCALE | (MODE == SM_BRIDGE ? (uint32_t)(SF_MID_EXPECT | SF_XSUM2 | SF_KEEP_V0)
+  constexpr uint32_t M0 = SF_POST_SCALE | (MODE == SM_BRIDGE ? (uint32_t)(SF_MID_EXPECT | SF_XSUM2 | SF_KEEP_V0)
                                           : NV == 1 ? (uint32_t)SF_MID_PHASE
                                                     : (uint32_t)(SF_XSUM | SF_MID_DINNER | SF_MID_PHASE | SF_XSUM2));
-  if ((a.flags & ~M) != 0) return invalid("internal: unexpected flags 0x%x for a merged sweep", a.flags);
+  static_assert(!STG || (NV == 2 && MODE == SM_MERGED), "the staggered schedule is a merged bra/ket sweep");
+  constexpr uint32_t M = M0 | (STG ? kStagBit : 0u);
+  if ((a.flags & ~M0) != 0) return invalid("internal: unexpected flags 0x%x for a merged sweep", a.flags);
   const bool c2 = a.form2 == GF_FACT_C;
   if constexpr (MODE == SM_BRIDGE) {  // Rx(-2b) then Rx(+2b): the same form
     if (a.shape == SA) return a.full ? L(SweepKernel<SA, NV, F1, false, true, MODE, F1, GR, M>{})
