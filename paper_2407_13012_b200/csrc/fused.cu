@@ -95,8 +95,9 @@ std::vector<SweepShape> plan_sweeps(int n) { return plan_range(n, 0, n - 1); }
 
 // Plain single-vector B sweeps run as lock-stepped 2-CTA clusters (256-byte DRAM runs;
 // +5% on those sweeps).  Merged and bra/ket sweeps, whose per-tile times vary more,
-// measured slower paired and stay unpaired.  QSB_PAIR=0 disables, =2 pairs every
-// single-vector B sweep (A/B tests).
+// measured slower paired and stay unpaired (re-measured with the relaxed cluster
+// barrier: still slower).  QSB_PAIR=0 disables, =2 pairs every single-vector B sweep,
+// =3 every B sweep (A/B tests).
 int pair_mode() {
   const char* e = getenv("QSB_PAIR");
   return e ? atoi(e) : 1;
@@ -375,7 +376,7 @@ struct Runner {
     a.mode = mode;
     {
       const int pm = pair_mode();
-      a.want_pair = (nv == 1 && ((pm == 1 && mode == SM_PLAIN) || pm == 2)) ? 1 : 0;
+      a.want_pair = ((nv == 1 && ((pm == 1 && mode == SM_PLAIN) || pm == 2)) || pm == 3) ? 1 : 0;
     }
     a.v0 = v0;
     a.v1 = v1;

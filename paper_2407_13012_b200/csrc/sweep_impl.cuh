@@ -207,6 +207,9 @@ constexpr uint32_t kStagBit = 1u << 30;
 #ifndef QSB_STAG_EARLY_STORE
 #define QSB_STAG_EARLY_STORE 1  // staggered sweeps store the lead during the lag's last stage
 #endif
+#ifndef QSB_PAIR_SYNC
+#define QSB_PAIR_SYNC 1  // paired B sweeps: 0 release/acquire lock-step, 1 relaxed lock-step, 2 one tile of slack
+#endif
 #ifndef QSB_EXCH_PRESYNC
 #define QSB_EXCH_PRESYNC 0  // 1: a CTA barrier before every warp-crossing exchange (A/B builds)
 #endif
@@ -760,10 +763,21 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
       if constexpr (GR == 2) issue(k + 3);
     }
    }  // k < my_tiles
-    if (a.pair) {
-      asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (a.pair) {  // no data crosses the pair: a relaxed arrive (no fence on this tile's stores)
+      if constexpr (QSB_PAIR_SYNC == 0) {
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+      } else if constexpr (QSB_PAIR_SYNC == 1) {
+        asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+      } else {  // one tile of slack: wait for the partner's previous tile, then arrive
+        if (k != (uint64_t)grp) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+      }
     }
+  }
+  if constexpr (QSB_PAIR_SYNC == 2) {
+    if (a.pair && iters > (uint64_t)grp) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   }
 
   // ------------------------------------------------------------ partial sums
