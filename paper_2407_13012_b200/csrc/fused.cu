@@ -103,19 +103,22 @@ int pair_mode() {
   return e ? atoi(e) : 1;
 }
 
-// register-bit family of the fast sweeps: 4 by default; overrides QSB_SWEEP_R1 /
-// QSB_SWEEP_R2 (plain sweeps, 3..6 / 3..4) and QSB_SWEEP_R1M (merged single-vector
-// sweeps, 4..6; merged bra/ket sweeps are R=4 only).  6 = the R=5 shapes with two
-// independent warp groups per CTA.
-int sweep_family(int nv, int mode) {
+// register-bit family of the fast sweeps (measured per window kind, n=30 chain):
+// single-vector plain sweeps 6 on A windows (two R=5 warp groups) and 4 on B windows
+// (R=4, paired clusters); single-vector merged sweeps 4 on A, 5 on B; bra/ket sweeps 4.
+// Overrides QSB_SWEEP_R1 / QSB_SWEEP_R2 (plain sweeps, 3..6 / 3..4), QSB_SWEEP_R1M
+// (merged single-vector sweeps, 4..6) and QSB_SWEEP_R2M (merged bra/ket: 3 or 4) apply
+// to both window kinds.  6 = the R=5 shapes with two independent warp groups per CTA.
+int sweep_family(int nv, int mode, bool is_a) {
   const bool merged = mode != SM_PLAIN;
   if (mode == SM_BRIDGE) return 4;
-  if (merged && nv == 2) {  // QSB_SWEEP_R2M: 3 (16 warps) or 4
+  if (merged && nv == 2) {
     const char* e2 = getenv("QSB_SWEEP_R2M");
     return (e2 && atoi(e2) == 3) ? 3 : 4;
   }
   const char* e = getenv(merged ? "QSB_SWEEP_R1M" : (nv == 1 ? "QSB_SWEEP_R1" : "QSB_SWEEP_R2"));
-  int r = e ? atoi(e) : 4;
+  if (!e) return nv == 2 ? 4 : merged ? (is_a ? 4 : 5) : (is_a ? 6 : 4);
+  int r = atoi(e);
   if (merged) return (r == 5 || r == 6) ? r : 4;
   if (nv == 2 && r >= 5) r = 4;  // two vectors of 32 amplitudes do not fit in registers
   if (r < 3 || r > 6) r = 4;
@@ -128,7 +131,7 @@ int build_shape(const SweepShape& sh, int n, int nv, bool exact, SweepArgs& a, i
                 int mode = SM_PLAIN) {
   int gl[kSweepT];
   for (int i = 0; i < kSweepT; ++i) gl[i] = sh.is_a ? i : (i < 3 ? i : sh.glo + i - 3);
-  const int fam = exact ? 4 : sweep_family(nv, mode);
+  const int fam = exact ? 4 : sweep_family(nv, mode, sh.is_a);
   const int shape = pick_shape(exact, sh.is_a, fam);
   a.groups = fam == 6 ? 2 : 1;
   const int np = shape_np(shape);
