@@ -27,6 +27,8 @@ int launch_sweep_m_nv2_r3_c(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_m_nv2_r3_s(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_m_nv2_t_c(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_m_nv2_t_s(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int launch_sweep_m_nv2_r3t_c(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int launch_sweep_m_nv2_r3t_s(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 
 // merged bra/ket sweeps: staggered schedule (default; QSB_STAG=0: lock-step)
 static bool stag_enabled() {
@@ -47,7 +49,10 @@ int launch_sweep(qsb_ctx* ctx, int nv, bool exact, SweepArgs& a, unsigned* gout)
       if (r == 5) return c ? launch_sweep_m_nv1_r5_c(ctx, a, gout) : launch_sweep_m_nv1_r5_s(ctx, a, gout);
       return c ? launch_sweep_m_nv1_r4_c(ctx, a, gout) : launch_sweep_m_nv1_r4_s(ctx, a, gout);
     }
-    if (r == 3) return c ? launch_sweep_m_nv2_r3_c(ctx, a, gout) : launch_sweep_m_nv2_r3_s(ctx, a, gout);
+    if (r == 3) {
+      if (stag_enabled()) return c ? launch_sweep_m_nv2_r3t_c(ctx, a, gout) : launch_sweep_m_nv2_r3t_s(ctx, a, gout);
+      return c ? launch_sweep_m_nv2_r3_c(ctx, a, gout) : launch_sweep_m_nv2_r3_s(ctx, a, gout);
+    }
     if (stag_enabled()) return c ? launch_sweep_m_nv2_t_c(ctx, a, gout) : launch_sweep_m_nv2_t_s(ctx, a, gout);
     return c ? launch_sweep_m_nv2_c(ctx, a, gout) : launch_sweep_m_nv2_s(ctx, a, gout);
   }
