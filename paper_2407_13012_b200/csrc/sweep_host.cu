@@ -23,6 +23,7 @@ int launch_sweep_nv1_r5g(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_m_nv2_c(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_m_nv2_s(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_bridge(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int launch_sweep_bridge_t(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_m_nv2_r3_c(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_m_nv2_r3_s(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_m_nv2_t_c(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
@@ -42,7 +43,10 @@ int launch_sweep(qsb_ctx* ctx, int nv, bool exact, SweepArgs& a, unsigned* gout)
     if (exact || a.form == GF_EXACT || a.shape != pick_shape(false, shape_is_a(a.shape), r) ||
         (nv == 1 && r == 3) || (nv == 2 && r == 5) || (a.mode == SM_BRIDGE && r != 4))
       return invalid("internal: merged sweeps are fast-mode; R=4 or R=5 (NV=1) / R=3 (NV=2) shapes");
-    if (a.mode == SM_BRIDGE) return nv == 2 ? launch_sweep_bridge(ctx, a, gout) : invalid("internal: bridge needs nv=2");
+    if (a.mode == SM_BRIDGE) {
+      if (nv != 2) return invalid("internal: bridge needs nv=2");
+      return stag_enabled() ? launch_sweep_bridge_t(ctx, a, gout) : launch_sweep_bridge(ctx, a, gout);
+    }
     const bool c = a.form == GF_FACT_C;
     if (nv == 1) {
       if (r == 5 && a.groups == 2) return c ? launch_sweep_m_nv1_r5g_c(ctx, a, gout) : launch_sweep_m_nv1_r5g_s(ctx, a, gout);

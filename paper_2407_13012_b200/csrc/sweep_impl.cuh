@@ -259,7 +259,9 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
   static_assert(GR == 1 || (GR == 2 && NV == 1), "warp groups: single-vector sweeps only");
   // staggered merged bra/ket sweep: the two vectors run half a stage apart, so one
   // vector's shared-memory exchange is in flight while the other's gates run
-  constexpr bool STAG = NV == 2 && MODE == SM_MERGED && GR == 1 && FM != 0xffffffffu && (FM & kStagBit) != 0;
+  // (bridge sweeps: the second pass only -- the first runs on the ket alone)
+  constexpr bool STAG = NV == 2 && MODE != SM_PLAIN && GR == 1 && FM != 0xffffffffu && (FM & kStagBit) != 0;
+  constexpr bool STAG1 = STAG && MODE == SM_MERGED;  // staggered from the first stage
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(smem_raw);
   const uint32_t cring_s = ring_s + kRing * kSlotBytes;
@@ -404,7 +406,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
 #pragma unroll
         for (int j = 0; j < NR; ++j) v[1][j] = lds(pb + (((uint32_t)j << P0.reg_l) * 16u));
       }
-      if constexpr (!STAG) {  // staggered: the ket lands in stage 0
+      if constexpr (!STAG1) {  // staggered: the ket lands in stage 0
         wait_seq(2 * k + 1);
         const uint32_t p0 = xs_addr + lb * 16u;
 #pragma unroll
@@ -546,7 +548,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
 
     // ---------------------------------------------------------------- pass 1
 #pragma unroll
-    for (int p = 0; p < (STAG ? 0 : NP); ++p) {
+    for (int p = 0; p < (STAG1 ? 0 : NP); ++p) {
       if (p > 0) exchange(shape_phase(SH, p - 1), shape_phase(SH, p), std::integral_constant<int, NVA>{});
       if (MODE == SM_PLAIN && p == NP - 1) release();
       // FULL: compile-time gate mask (no branches around the register tile)
@@ -674,6 +676,13 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
       };
       static_for<2 * NP>([&](auto sc) {
         constexpr int s = decltype(sc)::value;
+        if constexpr (MODE == SM_BRIDGE && s < NP) {  // pass 1 ran in lock-step on the ket
+          if constexpr (s == NP - 1) {
+            mid_ops(lb);
+            lb = lbase<W>(shape_phase(SH, 0), lane, warp);  // the tile ends in map P0 (stores)
+          }
+          return;
+        }
         constexpr int p = s < NP ? s : 2 * NP - 1 - s;
         constexpr PhaseSpec M = shape_phase(SH, p);
         // an exchange follows this stage unless it ends pass 1 (same map) or the sweep
@@ -902,7 +911,7 @@ int launch_merged_f1(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
   constexpr uint32_t M0 = SF_POST_SCALE | (MODE == SM_BRIDGE ? (uint32_t)(SF_MID_EXPECT | SF_XSUM2 | SF_KEEP_V0)
                                           : NV == 1 ? (uint32_t)SF_MID_PHASE
                                                     : (uint32_t)(SF_XSUM | SF_MID_DINNER | SF_MID_PHASE | SF_XSUM2));
-  static_assert(!STG || (NV == 2 && MODE == SM_MERGED), "the staggered schedule is a merged bra/ket sweep");
+  static_assert(!STG || (NV == 2 && MODE != SM_PLAIN), "the staggered schedule is a merged / bridge bra/ket sweep");
   constexpr uint32_t M = M0 | (STG ? kStagBit : 0u);
   if ((a.flags & ~M0) != 0) return invalid("internal: unexpected flags 0x%x for a merged sweep", a.flags);
   const bool c2 = a.form2 == GF_FACT_C;
