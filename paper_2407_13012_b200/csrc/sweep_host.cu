@@ -10,6 +10,7 @@ int launch_sweep_nv1_r5(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_nv1_r4(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_nv1_r3(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_nv2_r4(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int launch_sweep_nv2_r4t(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_nv2_r3(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_exact_nv1(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_exact_nv2(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
@@ -31,6 +32,12 @@ int launch_sweep_m_nv2_t_s(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_m_nv2_r3t_c(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_m_nv2_r3t_s(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 
+// plain bra/ket sweeps: staggered on A (bit 0) / B (bit 1) windows (QSB_STAGP; default
+// A only: on B windows the lock-step schedule measured the same)
+static int stagp_mask() {
+  const char* e = getenv("QSB_STAGP");
+  return e ? atoi(e) : 1;
+}
 // merged bra/ket sweeps: staggered schedule (default; QSB_STAG=0: lock-step)
 static bool stag_enabled() {
   const char* e = getenv("QSB_STAG");
@@ -66,6 +73,7 @@ int launch_sweep(qsb_ctx* ctx, int nv, bool exact, SweepArgs& a, unsigned* gout)
   if (nv == 1) return r == 5 ? launch_sweep_nv1_r5(ctx, a, gout) : r == 4 ? launch_sweep_nv1_r4(ctx, a, gout)
                                                                            : launch_sweep_nv1_r3(ctx, a, gout);
   if (r == 5) return invalid("internal: no R=5 bra/ket sweep");
+  if (r == 4 && (stagp_mask() & (shape_is_a(a.shape) ? 1 : 2))) return launch_sweep_nv2_r4t(ctx, a, gout);
   return r == 4 ? launch_sweep_nv2_r4(ctx, a, gout) : launch_sweep_nv2_r3(ctx, a, gout);
 }
 

@@ -204,6 +204,7 @@ __host__ __device__ constexpr bool stag_local(int sh, int p, int q) {
 // compile-time marker in a kernel's flag mask FM: run a merged bra/ket sweep with the
 // staggered schedule (see the kernel); never set in SweepArgs::flags
 constexpr uint32_t kStagBit = 1u << 30;
+constexpr uint32_t kStagFlags = 0x7fffffffu;  // every flag, staggered (plain sweeps)
 #ifndef QSB_STAG_EARLY_STORE
 #define QSB_STAG_EARLY_STORE 1  // staggered sweeps store the lead during the lag's last stage
 #endif
@@ -259,9 +260,11 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
   static_assert(GR == 1 || (GR == 2 && NV == 1), "warp groups: single-vector sweeps only");
   // staggered merged bra/ket sweep: the two vectors run half a stage apart, so one
   // vector's shared-memory exchange is in flight while the other's gates run
-  // (bridge sweeps: the second pass only -- the first runs on the ket alone)
-  constexpr bool STAG = NV == 2 && MODE != SM_PLAIN && GR == 1 && FM != 0xffffffffu && (FM & kStagBit) != 0;
+  // (bridge sweeps: the second pass only -- the first runs on the ket alone; plain
+  // sweeps: after the pre ops, which need both vectors at load)
+  constexpr bool STAG = NV == 2 && GR == 1 && !EXACT && FM != 0xffffffffu && (FM & kStagBit) != 0;
   constexpr bool STAG1 = STAG && MODE == SM_MERGED;  // staggered from the first stage
+  constexpr bool STAGP = STAG && MODE == SM_PLAIN;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(smem_raw);
   const uint32_t cring_s = ring_s + kRing * kSlotBytes;
@@ -548,7 +551,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
 
     // ---------------------------------------------------------------- pass 1
 #pragma unroll
-    for (int p = 0; p < (STAG1 ? 0 : NP); ++p) {
+    for (int p = 0; p < ((STAG1 || STAGP) ? 0 : NP); ++p) {
       if (p > 0) exchange(shape_phase(SH, p - 1), shape_phase(SH, p), std::integral_constant<int, NVA>{});
       if (MODE == SM_PLAIN && p == NP - 1) release();
       // FULL: compile-time gate mask (no branches around the register tile)
@@ -674,7 +677,11 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
 #pragma unroll
         for (int j = 0; j < NR; ++j) v[q][j] = lds(xa + (sn ^ (swz((uint32_t)j << P.reg_l) * 16u)));
       };
-      static_for<2 * NP>([&](auto sc) {
+      constexpr int NS = MODE == SM_PLAIN ? NP : 2 * NP;  // stages
+      // the stage at which the lag is already in registers (no load): after the pre ops
+      // (plain) or the mid ops (merged / bridge)
+      constexpr int SREG = MODE == SM_PLAIN ? 0 : NP;
+      static_for<NS>([&](auto sc) {
         constexpr int s = decltype(sc)::value;
         if constexpr (MODE == SM_BRIDGE && s < NP) {  // pass 1 ran in lock-step on the ket
           if constexpr (s == NP - 1) {
@@ -686,7 +693,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
         constexpr int p = s < NP ? s : 2 * NP - 1 - s;
         constexpr PhaseSpec M = shape_phase(SH, p);
         // an exchange follows this stage unless it ends pass 1 (same map) or the sweep
-        constexpr bool exch = s != NP - 1 && s != 2 * NP - 1;
+        constexpr bool exch = s != NP - 1 && s != NS - 1;
         constexpr int pn = s + 1 < NP ? s + 1 : 2 * NP - 2 - s;  // map of stage s+1
         constexpr bool loc = exch && stag_local<W>(SH, p, pn);
         const uint32_t apply = s < NP ? (FULL ? shape_apply(SH, p) : a.ph[p].apply)
@@ -697,18 +704,19 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
           else gate_vec<FORM2, NR, R>(v[q], apply, a.ga2, a.gb2);
         };
         gates(QLc{});
-        if constexpr (s == 0) {  // the lag lands (natural layout)
+        if constexpr (s == 0 && MODE == SM_MERGED) {  // the lag lands (natural layout)
           wait_seq(2 * k + 1);
           const uint32_t p0 = xs_addr + lb * 16u;
 #pragma unroll
           for (int j = 0; j < NR; ++j) v[0][j] = lds(p0 + (((uint32_t)j << M.reg_l) * 16u));
-        } else if constexpr (s != NP) {
+        } else if constexpr (s != SREG) {
           constexpr int pp = s - 1 < NP ? s - 1 : 2 * NP - s;  // map of stage s-1
           xload(QGc{}, M, std::integral_constant<bool, stag_local<W>(SH, pp, p)>{});
         }
         if constexpr (exch) xstore(QLc{}, M, std::integral_constant<bool, loc>{});
-        if constexpr (s == 2 * NP - 1) {
+        if constexpr (s == NS - 1) {
           release();  // the lag's last read: refill both slots
+          if constexpr (MODE == SM_PLAIN) lb = lbase<W>(M, lane, warp);  // the tile ends in this map
           // the lead is final: its stores drain while the lag is gated (scaled here, so
           // its last xsum weight is divided by the scale)
           if constexpr (QSB_STAG_EARLY_STORE) {
@@ -717,16 +725,16 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
           }
         }
         gates(QGc{});
+        double w = s < NP ? a.xs_w[p] : a.xs_w2[p];
+        if constexpr (s == NS - 1 && QSB_STAG_EARLY_STORE) {
+          if (!EXACT && (flags & SF_POST_SCALE)) w /= a.post_scale;
+        }
         if constexpr (s < NP) {
-          if (flags & SF_XSUM) xsum(acc2, a.xs_w[p], apply);
+          if (flags & SF_XSUM) xsum(acc2, w, apply);
         } else {
-          double w = a.xs_w2[p];
-          if constexpr (s == 2 * NP - 1 && QSB_STAG_EARLY_STORE) {
-            if (!EXACT && (flags & SF_POST_SCALE)) w /= a.post_scale;
-          }
           if (flags & SF_XSUM2) xsum(acc3, w, apply);
         }
-        if constexpr (s == NP - 1) mid_ops(lbase<W>(M, lane, warp));
+        if constexpr (s == NP - 1 && MODE == SM_MERGED) mid_ops(lbase<W>(M, lane, warp));
         if constexpr (exch) {
           xload(QLc{}, shape_phase(SH, pn), std::integral_constant<bool, loc>{});
           xstore(QGc{}, M, std::integral_constant<bool, loc>{});
@@ -872,8 +880,8 @@ struct SweepKernel {
 };
 
 // fast-mode instantiations of one register family (A shape SA, B shape SB, GR warp
-// groups).  A sweeps always cover their whole 12-bit window; B windows may be partial.
-template <int NV, int SA, int SB, int GR = 1>
+// groups; FMX = kStagFlags: the staggered bra/ket schedule).  A sweeps always cover their whole 12-bit window; B windows may be partial.
+template <int NV, int SA, int SB, int GR = 1, uint32_t FMX = 0xffffffffu>
 int launch_fast(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
   auto L = [&](auto k) { return decltype(k)::launch(ctx, a, g); };
   const bool ksin = a.kind == 0;
@@ -892,14 +900,14 @@ int launch_fast(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
   }
   if (a.shape == SA) {
     if (!a.full) {  // partial A windows (sharded tails below bit 12): runtime masks
-      if (c) return ksin ? L(SweepKernel<SA, NV, C, true, false, P, C, GR>{}) : L(SweepKernel<SA, NV, C, false, false, P, C, GR>{});
-      return ksin ? L(SweepKernel<SA, NV, S, true, false, P, S, GR>{}) : L(SweepKernel<SA, NV, S, false, false, P, S, GR>{});
+      if (c) return ksin ? L(SweepKernel<SA, NV, C, true, false, P, C, GR, FMX>{}) : L(SweepKernel<SA, NV, C, false, false, P, C, GR, FMX>{});
+      return ksin ? L(SweepKernel<SA, NV, S, true, false, P, S, GR, FMX>{}) : L(SweepKernel<SA, NV, S, false, false, P, S, GR, FMX>{});
     }
-    if (c) return ksin ? L(SweepKernel<SA, NV, C, true, true, P, C, GR>{}) : L(SweepKernel<SA, NV, C, false, true, P, C, GR>{});
-    return ksin ? L(SweepKernel<SA, NV, S, true, true, P, S, GR>{}) : L(SweepKernel<SA, NV, S, false, true, P, S, GR>{});
+    if (c) return ksin ? L(SweepKernel<SA, NV, C, true, true, P, C, GR, FMX>{}) : L(SweepKernel<SA, NV, C, false, true, P, C, GR, FMX>{});
+    return ksin ? L(SweepKernel<SA, NV, S, true, true, P, S, GR, FMX>{}) : L(SweepKernel<SA, NV, S, false, true, P, S, GR, FMX>{});
   }
-  if (a.full) return c ? L(SweepKernel<SB, NV, C, false, true, P, C, GR>{}) : L(SweepKernel<SB, NV, S, false, true, P, S, GR>{});
-  return c ? L(SweepKernel<SB, NV, C, false, false, P, C, GR>{}) : L(SweepKernel<SB, NV, S, false, false, P, S, GR>{});
+  if (a.full) return c ? L(SweepKernel<SB, NV, C, false, true, P, C, GR, FMX>{}) : L(SweepKernel<SB, NV, S, false, true, P, S, GR, FMX>{});
+  return c ? L(SweepKernel<SB, NV, C, false, false, P, C, GR, FMX>{}) : L(SweepKernel<SB, NV, S, false, false, P, S, GR, FMX>{});
 }
 
 // merged / bridge instantiations (fast mode; shapes SA / SB of one register family).  Table ops between
