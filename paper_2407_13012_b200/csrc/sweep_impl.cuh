@@ -96,6 +96,18 @@ __device__ __forceinline__ void tma_5d(uint32_t dst, const CUtensorMap* map, int
       : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// TMA stores (bulk groups of the issuing thread)
+__device__ __forceinline__ void tma_store_1d(void* dst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, int c1, int c4, uint32_t src) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(map),
+               "r"(0), "r"(c1), "r"(0), "r"(0), "r"(c4), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ uint64_t tile_base(const SweepArgs& a, uint64_t tile) {
@@ -211,6 +223,9 @@ constexpr uint32_t kStagFlags = 0x7fffffffu;  // every flag, staggered (plain sw
 #ifndef QSB_PAIR_SYNC
 #define QSB_PAIR_SYNC 1  // paired B sweeps: 0 release/acquire lock-step, 1 relaxed lock-step, 2 one tile of slack
 #endif
+#ifndef QSB_TMA_STORE
+#define QSB_TMA_STORE 1  // single-vector A sweeps (one warp group) store their tiles with TMA
+#endif
 #ifndef QSB_EXCH_PRESYNC
 #define QSB_EXCH_PRESYNC 0  // 1: a CTA barrier before every warp-crossing exchange (A/B builds)
 #endif
@@ -265,6 +280,10 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
   constexpr bool STAG = NV == 2 && GR == 1 && !EXACT && FM != 0xffffffffu && (FM & kStagBit) != 0;
   constexpr bool STAG1 = STAG && MODE == SM_MERGED;  // staggered from the first stage
   constexpr bool STAGP = STAG && MODE == SM_PLAIN;
+  // single-vector A tiles leave through shared memory and a 1-D TMA store (no per-thread
+  // global stores holding registers); the slot is reloaded once the store has read it.
+  // (B tiles measured slower with 5-D tensor stores of 128-byte runs.)
+  constexpr bool TMAST = QSB_TMA_STORE && NV == 1 && GR == 1 && IS_A;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(smem_raw);
   const uint32_t cring_s = ring_s + kRing * kSlotBytes;
@@ -312,6 +331,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
   // even = bra (v1) of tile s/2, odd = ket (v0).
   auto issue = [&](uint64_t s) {
     if (tid != 0 || s >= nseq) return;
+    if constexpr (TMAST) bulk_wait_read0();  // the slot's previous tile has left
     const uint64_t k = s / NV;
     const int q = NV == 2 ? (int)((s & 1) ^ 1) : 0;
     const uint64_t tile = blockIdx.x + k * gridDim.x;
@@ -390,7 +410,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     // Loads are unconditional (a skipped TMA leaves stale data that is overwritten
     // below): no branch around the register tile, hence no phi-moves of it.
     if constexpr (NV == 1) {
-      if constexpr (GR == 1) issue(k + 2);
+      if constexpr (GR == 1 && !TMAST) issue(k + 2);  // (TMAST: after the first phase)
       wait_seq(k);
       xs_addr = ring_s + (uint32_t)(k % kRing) * kSlotBytes;
       const uint32_t p0 = xs_addr + lb * 16u;  // natural (TMA) layout
@@ -553,6 +573,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
 #pragma unroll
     for (int p = 0; p < ((STAG1 || STAGP) ? 0 : NP); ++p) {
       if (p > 0) exchange(shape_phase(SH, p - 1), shape_phase(SH, p), std::integral_constant<int, NVA>{});
+      if (TMAST && p == 1) issue(k + 2);  // tile k-1's store has long read its slot
       if (MODE == SM_PLAIN && p == NP - 1) release();
       // FULL: compile-time gate mask (no branches around the register tile)
       const uint32_t apply = FULL ? shape_apply(SH, p) : a.ph[p].apply;
@@ -767,8 +788,17 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     // NV=1: order this tile's generic-proxy smem writes (exchanges) before the TMA that
     // will refill the slot.  Fenced here, ahead of the global stores: the fence's
     // MEMBAR then does not wait for this tile's 64 KB of stores to drain.
+    const bool tma_out = TMAST && a.sw_g == 0 && !(flags & SF_NO_STORE);
+    if (tma_out) {
+      // natural layout (the final map puts quarter-warp lanes on local bits 0..2:
+      // conflict-free, and each 8-amplitude chunk is the warp's own -- a warp barrier
+      // orders it after the last exchange's reads)
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < NR; ++j) sts(xs_addr + (lb | ((uint32_t)j << RL)) * 16u, v[0][j]);
+    }
     if constexpr (NV == 1) fence_proxy_async();
-    if (!(flags & SF_NO_STORE)) {
+    if (!(flags & SF_NO_STORE) && !tma_out) {
 #pragma unroll
       for (int q = Q0; q < Q1; ++q) {
         if (q == 0 && MODE == SM_BRIDGE && (flags & SF_KEEP_V0)) continue;
@@ -776,7 +806,19 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
       }
     }
     if constexpr (NV == 1) {
-      gsync();  // the slot may be refilled from here on
+      gsync();  // the slot may be refilled from here on (TMAST: once the store has read it)
+      if constexpr (TMAST) {
+        if (tma_out && tid == 0) {
+          const uint64_t tile = blockIdx.x + k * gridDim.x;
+          if constexpr (IS_A) {
+            tma_store_1d(a.v0 + (tile << kSweepT), xs_addr, kSlotBytes);
+          } else {
+            const int lowbits = glo - 3;
+            tma_store_5d(&a.tm0, (int)(tile & ((1ull << lowbits) - 1ull)), (int)(tile >> lowbits), xs_addr);
+          }
+          bulk_commit();
+        }
+      }
       if constexpr (GR == 2) issue(k + 3);
     }
    }  // k < my_tiles
@@ -795,6 +837,10 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
   }
   if constexpr (QSB_PAIR_SYNC == 2) {
     if (a.pair && iters > (uint64_t)grp) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  }
+
+  if constexpr (TMAST) {
+    if (tid == 0) bulk_wait0();  // the tiles are in global memory before the kernel ends
   }
 
   // ------------------------------------------------------------ partial sums
