@@ -226,6 +226,9 @@ constexpr uint32_t kStagFlags = 0x7fffffffu;  // every flag, staggered (plain sw
 #ifndef QSB_TMA_STORE
 #define QSB_TMA_STORE 1  // single-vector A sweeps (one warp group) store their tiles with TMA
 #endif
+#ifndef QSB_TMA_STORE_B
+#define QSB_TMA_STORE_B 0  // 1: B tiles too (5-D tensor stores)
+#endif
 #ifndef QSB_EXCH_PRESYNC
 #define QSB_EXCH_PRESYNC 0  // 1: a CTA barrier before every warp-crossing exchange (A/B builds)
 #endif
@@ -283,7 +286,10 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
   // single-vector A tiles leave through shared memory and a 1-D TMA store (no per-thread
   // global stores holding registers); the slot is reloaded once the store has read it.
   // (B tiles measured slower with 5-D tensor stores of 128-byte runs.)
-  constexpr bool TMAST = QSB_TMA_STORE && NV == 1 && GR == 1 && IS_A;
+  constexpr bool TMAST = QSB_TMA_STORE && NV == 1 && GR == 1 && (IS_A || QSB_TMA_STORE_B);
+  // the next load into a slot waits for the slot's store to be read: A tiles issue it
+  // after the first phase, B tiles (slow strided loads) at the tile start
+  constexpr bool LATE_ISSUE = TMAST && IS_A;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(smem_raw);
   const uint32_t cring_s = ring_s + kRing * kSlotBytes;
@@ -410,7 +416,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     // Loads are unconditional (a skipped TMA leaves stale data that is overwritten
     // below): no branch around the register tile, hence no phi-moves of it.
     if constexpr (NV == 1) {
-      if constexpr (GR == 1 && !TMAST) issue(k + 2);  // (TMAST: after the first phase)
+      if constexpr (GR == 1 && !LATE_ISSUE) issue(k + 2);  // (LATE_ISSUE: after the first phase)
       wait_seq(k);
       xs_addr = ring_s + (uint32_t)(k % kRing) * kSlotBytes;
       const uint32_t p0 = xs_addr + lb * 16u;  // natural (TMA) layout
@@ -573,7 +579,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
 #pragma unroll
     for (int p = 0; p < ((STAG1 || STAGP) ? 0 : NP); ++p) {
       if (p > 0) exchange(shape_phase(SH, p - 1), shape_phase(SH, p), std::integral_constant<int, NVA>{});
-      if (TMAST && p == 1) issue(k + 2);  // tile k-1's store has long read its slot
+      if (LATE_ISSUE && p == 1) issue(k + 2);  // tile k-1's store has long read its slot
       if (MODE == SM_PLAIN && p == NP - 1) release();
       // FULL: compile-time gate mask (no branches around the register tile)
       const uint32_t apply = FULL ? shape_apply(SH, p) : a.ph[p].apply;
