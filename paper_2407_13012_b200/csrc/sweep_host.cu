@@ -11,6 +11,7 @@ int launch_sweep_nv1_r4(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_nv1_r3(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_nv2_r4(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_nv2_r4t(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
+int launch_sweep_nv2_r3t(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_nv2_r3(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_exact_nv1(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
 int launch_sweep_exact_nv2(qsb_ctx* ctx, SweepArgs& a, unsigned* g);
@@ -73,7 +74,7 @@ int launch_sweep(qsb_ctx* ctx, int nv, bool exact, SweepArgs& a, unsigned* gout)
   if (nv == 1) return r == 5 ? launch_sweep_nv1_r5(ctx, a, gout) : r == 4 ? launch_sweep_nv1_r4(ctx, a, gout)
                                                                            : launch_sweep_nv1_r3(ctx, a, gout);
   if (r == 5) return invalid("internal: no R=5 bra/ket sweep");
-  if (r == 4 && (stagp_mask() & (shape_is_a(a.shape) ? 1 : 2))) return launch_sweep_nv2_r4t(ctx, a, gout);
+  if (stagp_mask() & (shape_is_a(a.shape) ? 1 : 2)) return r == 4 ? launch_sweep_nv2_r4t(ctx, a, gout) : launch_sweep_nv2_r3t(ctx, a, gout);
   return r == 4 ? launch_sweep_nv2_r4(ctx, a, gout) : launch_sweep_nv2_r3(ctx, a, gout);
 }
 
