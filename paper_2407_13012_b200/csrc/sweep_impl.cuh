@@ -1,5 +1,6 @@
 // The fused sweep kernel — the hot path of every forward and backward layer.
-// (Instantiated in sweep_nv1.cu / sweep_nv2.cu; descriptor in sweep.cuh.)
+// (Instantiated per family in sweep_nv*.cu / sweep_m_*.cu / sweep_bridge.cu /
+// sweep_exact.cu; descriptor in sweep.cuh; dispatch in sweep_host.cu.)
 //
 // One launch streams the whole statevector (or the bra/ket pair) through HBM once.
 // A CTA owns 2^12-amplitude tiles whose 12 "local" bits map to global index bits
@@ -21,7 +22,10 @@
 // the next one or two vector-tiles are in flight (128 KB per SM).  The landed
 // tile is read in the natural layout (every shape's first phase puts quarter-warp
 // lanes on local bits 0..2: conflict-free), exchanges use the swizzled layout,
-// and results go straight from registers to HBM with coalesced 16-byte stores.
+// and results go straight from registers to HBM with coalesced 16-byte stores
+// (single-vector A tiles: back through the slot and out with one TMA bulk store).
+// Bra/ket sweeps can run the two vectors half a stage apart (the staggered schedule,
+// flag-mask bit kStagBit) so one vector's exchange overlaps the other's gates.
 //
 // Fused ops: the cost phase exp(-i*gamma*C) (compact index -> LUT, the index tile
 // rides the A-tile TMA), bra = C*ket, <bra|C|ket>, sum_j <bra|X_j|ket> (before each
