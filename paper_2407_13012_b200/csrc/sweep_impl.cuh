@@ -233,6 +233,9 @@ constexpr uint32_t kStagFlags = 0x7fffffffu;  // every flag, staggered (plain sw
 #ifndef QSB_TMA_STORE_B
 #define QSB_TMA_STORE_B 0  // 1: B tiles too (5-D tensor stores)
 #endif
+#ifndef QSB_STAG_ARRIVE_ALL
+#define QSB_STAG_ARRIVE_ALL 1  // every thread arrives on the exchange mbarriers (0: one elected lane per warp after a __syncwarp -- same speed, but compute-sanitizer racecheck cannot follow it)
+#endif
 #ifndef QSB_EXCH_PRESYNC
 #define QSB_EXCH_PRESYNC 0  // 1: a CTA barrier before every warp-crossing exchange (A/B builds)
 #endif
@@ -313,8 +316,8 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
 #pragma unroll
     for (int s = 0; s < GR * kRing; ++s) mbar_init(bar_s + 8 * s, 1);
     if constexpr (STAG) {  // exchange barriers of the two vectors: one arrival per warp
-      mbar_init(bar_s + 8 * 6, 1u << W);
-      mbar_init(bar_s + 8 * 7, 1u << W);
+      mbar_init(bar_s + 8 * 6, QSB_STAG_ARRIVE_ALL ? NT : 1u << W);
+      mbar_init(bar_s + 8 * 7, QSB_STAG_ARRIVE_ALL ? NT : 1u << W);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -691,8 +694,12 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
 #pragma unroll
         for (int j = 0; j < NR; ++j) sts(xa + (so ^ (swz((uint32_t)j << Q.reg_l) * 16u)), v[q][j]);
         if constexpr (!decltype(localc)::value) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(bar_s + 8u * (6u + (uint32_t)q));
+          if constexpr (QSB_STAG_ARRIVE_ALL) {
+            mbar_arrive(bar_s + 8u * (6u + (uint32_t)q));
+          } else {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_s + 8u * (6u + (uint32_t)q));
+          }
         }
       };
       auto xload = [&](auto qc, const PhaseSpec P, auto localc) {
