@@ -229,6 +229,21 @@ int qsb_sample_tree(qsb_ctx* ctx, const double* amps, int n_local, double* root_
 int qsb_sample_descend(qsb_ctx* ctx, qsb_table* t, const double* amps, int n_local, uint64_t count, const double* u,
                        int64_t* idx_out, double* cost_out);
 
+/* Standalone qubit swap of a sharded statevector (SURVEY.md §8(e) "The collective";
+ * no reference counterpart -- the reference is single-array): chunk c
+ * (chunk_amps amplitudes at src + c * chunk_amps) goes to dsts[c] + dst_off_amps, for
+ * c < nchunks <= 8, in one kernel.  dsts may be CUDA-IPC-mapped peer buffers (the
+ * stores cross NVLink; complete with qsb_device_sync + a host barrier). */
+int qsb_scatter_chunks(qsb_ctx* ctx, const double* src, uint64_t chunk_amps, int nchunks, void* const* dsts,
+                       uint64_t dst_off_amps);
+/* amps[i] = re + i*im (a shard's part of |+> is 1/sqrt(2^n_global), fill_plus
+ * numba_impl.py:40-44 for the whole register) */
+int qsb_fill_const(qsb_ctx* ctx, double* amps, uint64_t len, double re, double im);
+/* Drop the table's fp64 values (kind 1/2 only): every later use reads the compact
+ * index (T = vmin + idx, exact for integral tables).  Lets a sharded handle free the
+ * 8 B/amp fp64 copy of each layout's table (the caller frees the memory). */
+int qsb_table_detach_values(qsb_table* t);
+
 #ifdef __cplusplus
 }
 #endif

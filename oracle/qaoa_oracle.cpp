@@ -8,8 +8,8 @@
  * arithmetic is the numba set's (no FMA contraction, same cos/sin), which makes
  * its outputs bit-identical to the reference; tests/test_oracle_golden.py pins
  * it against golden vectors produced by the reference itself
- * (tests/golden/make_golden.py).  Parallel loops use std::thread (static
- * chunks); reductions keep the reference's neighbour-pair association, so the
+ * (tests/golden/make_golden.py).  Parallel loops run on a persistent std::thread
+ * pool (static chunks); reductions keep the reference's neighbour-pair association, so the
  * thread count never changes a result.
  *
  * Each function cites the reference source it restates
@@ -21,6 +21,10 @@
 #include <string.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <functional>
+#include <memory>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -38,25 +42,90 @@ int threads_now() {
   return h ? (int)h : 1;
 }
 
+// Persistent worker pool (like numba's workqueue layer, numba_impl.py:24, the
+// reference's threads live across kernel calls): spawning threads per call would
+// add tens of microseconds to each of the reference's ~10^3 whole-array passes.
+class Pool {
+ public:
+  explicit Pool(int workers) {
+    for (int t = 1; t <= workers; ++t) th_.emplace_back([this, t] { loop(t); });
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int size() const { return (int)th_.size() + 1; }
+  // job(t) for t in [0, size()): the caller runs t = 0
+  void run(const std::function<void(int)>& job) {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      job_ = &job;
+      pending_ = (int)th_.size();
+      ++gen_;
+    }
+    cv_.notify_all();
+    job(0);
+    std::unique_lock<std::mutex> g(m_);
+    done_.wait(g, [this] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void loop(int t) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* job;
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+        job = job_;
+      }
+      (*job)(t);
+      std::lock_guard<std::mutex> g(m_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  uint64_t gen_ = 0;
+  int pending_ = 0;
+  bool stop_ = false;
+};
+
+Pool& pool() {
+  static std::unique_ptr<Pool> p;
+  static int size = 0;
+  const int T = threads_now();
+  if (!p || size != T) {
+    p.reset();
+    p.reset(new Pool(T - 1));
+    size = T;
+  }
+  return *p;
+}
+
 // static-schedule parallel loop: f(i) for i in [0, n)
 template <class F>
 void parallel_for(int64_t n, F f) {
   const int T = threads_now();
-  auto run = [&f](int64_t lo, int64_t hi) {
-    for (int64_t i = lo; i < hi; ++i) f(i);
-  };
   if (T <= 1 || n < 16384) {
-    run(0, n);
+    for (int64_t i = 0; i < n; ++i) f(i);
     return;
   }
-  std::vector<std::thread> pool;
   const int64_t chunk = (n + T - 1) / T;
-  for (int t = 0; t < T; ++t) {
+  pool().run([&](int t) {
     const int64_t lo = t * chunk, hi = std::min<int64_t>(n, lo + chunk);
-    if (lo >= hi) break;
-    pool.emplace_back(run, lo, hi);
-  }
-  for (auto& th : pool) th.join();
+    for (int64_t i = lo; i < hi; ++i) f(i);
+  });
 }
 
 constexpr uint64_t BLOCK = 2048;  // numba_impl.py:26 (any power of two gives the same tree)

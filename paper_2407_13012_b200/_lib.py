@@ -93,6 +93,9 @@ _SIGS = {
     "qsb_device_sync": [_vp],
     "qsb_small_batch": [_vp, _i32, _vp, _vp, _vp, _dp, _dp, _i32, _dp],
     "qsb_sample_descend": [_vp, _vp, _vp, _i32, _u64, _vp, _vp, _vp],
+    "qsb_scatter_chunks": [_vp, _vp, _u64, _i32, _vp, _u64],
+    "qsb_fill_const": [_vp, _vp, _u64, _dbl, _dbl],
+    "qsb_table_detach_values": [_vp],
 }
 _RESTYPES = {"qsb_last_error": C.c_char_p, "qsb_abi_version": _i32}
 
@@ -280,6 +283,9 @@ class DeviceArray:
             raise ContractViolation("use of a freed device buffer")
         arr = np.ascontiguousarray(np.broadcast_to(np.asarray(values, dtype=self.dtype), (self.length,)))
         call("qsb_h2d", self.dctx.handle, self.ptr, arr.ctypes.data, self.nbytes)
+        # a cost table written from the host: its cached compact index / LUT metadata
+        # (qsb_table) is stale -- rebuilt from the new values on next use
+        self.table = None
 
     def __array__(self, dtype=None, copy=None):
         host = self.to_host()

@@ -44,11 +44,15 @@ def _walk(handle: circuit.SimHandle, params: circuit.QaoaParams, want_value: boo
     bra = handle._adjoint_state()
     try:
         value, dg, db = handle.ctx.kernels.value_and_grad(
-            handle.state.data, bra.data, handle.table.values.data, handle.n, params.gammas, params.betas,
+            handle.state.overwrite_target(), bra.data, handle.table.values.data, handle.n, params.gammas, params.betas,
             exact=backend.exact_mode(), want_value=want_value,
         )
     finally:
         bra.free()
+    if not backend.exact_mode() and handle.n >= 12:
+        # the fused walk's last sweep only contracts: the ket is |+> by contract (the
+        # reference's gradient leaves it there), written lazily on the next read
+        handle.state.mark_plus()
     n = handle.n
     # reference-equivalent instrumentation: forward, bra prep, 4p inverse layers, reductions
     levels = backend._reduction_levels(1 << n)

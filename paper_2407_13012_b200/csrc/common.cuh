@@ -88,6 +88,21 @@ struct qsb_table {
 };
 
 namespace qsb {
+// Kernel function attributes (max dynamic shared memory) and occupancy are per
+// device: one-time setup is cached per device ordinal, not per process, so a kernel
+// first launched on one GPU still gets its attributes on another.
+constexpr int kMaxDevices = 64;
+template <class T>
+struct PerDevice {
+  std::once_flag once[kMaxDevices];
+  T val[kMaxDevices];
+  template <class F>
+  const T& get(int dev, F&& init) {
+    const int d = dev < 0 || dev >= kMaxDevices ? 0 : dev;
+    std::call_once(once[d], [&] { val[d] = init(); });
+    return val[d];
+  }
+};
 // profiling hooks (no-ops unless ctx->prof)
 int prof_mark(qsb_ctx* ctx, cudaEvent_t* ev);
 int ensure_scratch(qsb_ctx* ctx, uint64_t bytes);

@@ -711,6 +711,7 @@ extern "C" {
 // around the index-bit swap.
 int qsb_layer_sweeps(qsb_ctx* ctx, qsb_table* t, double* v0, double* v1, int nv, int n, int n_global, int lo,
                      int hi, double theta, unsigned flags, double phase_scale, double* sums) {
+  if (ctx) QSB_CUDA(cudaSetDevice(ctx->device));  // launches go to the context's GPU
   if (!ctx || !t || !v0 || (nv == 2 && !v1) || !sums) return invalid("qsb_layer_sweeps: null argument");
   if (nv != 1 && nv != 2) return invalid("qsb_layer_sweeps: nv must be 1 or 2");
   if (n < kSweepT || n > 62 || n != t->n) return invalid("qsb_layer_sweeps: n=%d (table n=%d, need >= 12)", n, t->n);
@@ -752,6 +753,7 @@ int qsb_layer_sweeps(qsb_ctx* ctx, qsb_table* t, double* v0, double* v1, int nv,
 
 int qsb_shard_visit_run(qsb_ctx* ctx, qsb_table* t, double* v0, double* v1, int n, int n_global,
                         const qsb_shard_visit* d, double* sums) {
+  if (ctx) QSB_CUDA(cudaSetDevice(ctx->device));  // launches go to the context's GPU
   if (!ctx || !t || !v0 || !d || !sums || (d->nv == 2 && !v1)) return invalid("qsb_shard_visit_run: null argument");
   if (d->nv != 1 && d->nv != 2) return invalid("qsb_shard_visit_run: nv must be 1 or 2");
   if (n < kSweepT || n > 62 || n != t->n) return invalid("qsb_shard_visit_run: n=%d (table n=%d, need >= 12)", n, t->n);
@@ -803,6 +805,7 @@ int qsb_shard_visit_run(qsb_ctx* ctx, qsb_table* t, double* v0, double* v1, int 
 extern "C" {
 
 int qsb_rx_layer(qsb_ctx* ctx, double* amps, int n, double theta, unsigned flags) {
+  if (ctx) QSB_CUDA(cudaSetDevice(ctx->device));  // launches go to the context's GPU
   if (!ctx || !amps) return invalid("qsb_rx_layer: null argument");
   if (n < 1 || n > 62) return invalid("qsb_rx_layer: n=%d out of range", n);
   const bool exact = flags & QSB_EXACT;
@@ -818,6 +821,7 @@ int qsb_rx_layer(qsb_ctx* ctx, double* amps, int n, double theta, unsigned flags
 // simulate with optional fused expectation (expect_out != NULL)
 int qsb_simulate_expect(qsb_ctx* ctx, qsb_table* t, double* amps, int p, const double* gammas, const double* betas,
                         unsigned flags, double* expect_out) {
+  if (ctx) QSB_CUDA(cudaSetDevice(ctx->device));  // launches go to the context's GPU
   if (!ctx || !t || !amps) return invalid("qsb_simulate: null argument");
   if (p < 0 || (p > 0 && (!gammas || !betas))) return invalid("qsb_simulate: bad parameters");
   const bool exact = flags & QSB_EXACT;
@@ -902,6 +906,7 @@ static int value_and_grad_perop(qsb_ctx* ctx, qsb_table* t, double2* ket, double
 int qsb_value_and_grad(qsb_ctx* ctx, qsb_table* t, double* ket_, double* bra_, int p, const double* gammas,
                        const double* betas, unsigned flags, int skip_forward, double* value, double* d_gammas,
                        double* d_betas) {
+  if (ctx) QSB_CUDA(cudaSetDevice(ctx->device));  // launches go to the context's GPU
   if (!ctx || !t || !ket_ || !bra_ || !d_gammas || !d_betas) return invalid("qsb_value_and_grad: null argument");
   if (p < 1) return invalid("gradient needs depth p >= 1");
   if (!gammas || !betas) return invalid("qsb_value_and_grad: null parameters");

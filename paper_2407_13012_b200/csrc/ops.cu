@@ -313,6 +313,7 @@ int xsum_exact(qsb_ctx* ctx, const double2* a, const double2* b, uint64_t len, i
 extern "C" {
 
 int qsb_fill_plus(qsb_ctx* ctx, double* amps, uint64_t len) {
+  if (ctx) QSB_CUDA(cudaSetDevice(ctx->device));  // launches go to the context's GPU
   if (!ctx || !amps) return invalid("qsb_fill_plus: null argument");
   if (!len) return QSB_OK;
   return launch_fill_plus(ctx, (double2*)amps, len);

@@ -109,9 +109,23 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+// the cost of a drawn index: the fp64 table, or (a sharded table whose fp64 copy was
+// dropped, qsb_table_detach_values) the compact index: T = vmin + idx, exact for the
+// integral tables that have one
+struct CostView {
+  const double* values;
+  const void* cidx;
+  int kind;
+  double vmin;
+  __device__ double at(uint64_t i) const {
+    if (values) return values[i];
+    return vmin + (double)(kind == 1 ? ((const uint8_t*)cidx)[i] : ((const uint16_t*)cidx)[i]);
+  }
+};
+
 // u_in == nullptr: u_s = U(seed, s) * root (the reference's draw); else u_s = u_in[s]
 // (a shard's residuals after the caller descended the levels above it).
-__global__ void k_descend(const double2* __restrict__ amps, Levels L, const double* __restrict__ table, uint64_t shots,
+__global__ void k_descend(const double2* __restrict__ amps, Levels L, const CostView table, uint64_t shots,
                           uint64_t seed, double root, const double* __restrict__ u_in, int64_t* __restrict__ idx_out,
                           double* __restrict__ cost_out) {
   for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < shots; s += (uint64_t)gridDim.x * blockDim.x) {
@@ -161,7 +175,7 @@ __global__ void k_descend(const double2* __restrict__ amps, Levels L, const doub
     }
     idx = leaf0 + loc;
     idx_out[s] = (int64_t)idx;
-    if (table) cost_out[s] = table[idx];
+    if (cost_out) cost_out[s] = table.at(idx);
   }
 }
 
@@ -201,8 +215,9 @@ int descend(qsb_ctx* ctx, qsb_table* t, const double2* a, const Levels& L, uint6
   }
   uint64_t blocks = (shots + 255) / 256;
   if (blocks > (uint64_t)ctx->num_sms * 64) blocks = (uint64_t)ctx->num_sms * 64;
-  k_descend<<<(unsigned)blocks, 256, 0, ctx->stream>>>(a, L, t ? t->values : nullptr, shots, seed, root, d_u, d_idx,
-                                                        t ? d_cost : nullptr);
+  const CostView cv{t ? t->values : nullptr, t ? t->cidx : nullptr, t ? t->kind : 0, t ? t->vmin : 0.0};
+  if (t && !t->values && !t->cidx) return invalid("sampling: the table has neither fp64 values nor a compact index");
+  k_descend<<<(unsigned)blocks, 256, 0, ctx->stream>>>(a, L, cv, shots, seed, root, d_u, d_idx, t ? d_cost : nullptr);
   QSB_CHECK_LAUNCH(ctx, "sample descent");
   QSB_CUDA(cudaMemcpyAsync(idx_out, d_idx, shots * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
   if (t) QSB_CUDA(cudaMemcpyAsync(cost_out, d_cost, shots * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -217,6 +232,7 @@ extern "C" {
 
 int qsb_sample(qsb_ctx* ctx, qsb_table* t, const double* amps, int n, uint64_t shots, uint64_t seed,
                int64_t* idx_out, double* cost_out, double* total_out) {
+  if (ctx) QSB_CUDA(cudaSetDevice(ctx->device));  // launches go to the context's GPU
   if (!ctx || !amps || !idx_out) return invalid("qsb_sample: null argument");
   if (shots < 1) return invalid("shots must be >= 1, got %llu", (unsigned long long)shots);
   if (n < 1 || n > 62) return invalid("qsb_sample: n=%d out of range", n);
@@ -233,6 +249,7 @@ int qsb_sample(qsb_ctx* ctx, qsb_table* t, const double* amps, int n, uint64_t s
 }
 
 int qsb_sample_tree(qsb_ctx* ctx, const double* amps, int n_local, double* root_out) {
+  if (ctx) QSB_CUDA(cudaSetDevice(ctx->device));  // launches go to the context's GPU
   if (!ctx || !amps || !root_out) return invalid("qsb_sample_tree: null argument");
   if (n_local < 1 || n_local > 62) return invalid("qsb_sample_tree: n=%d out of range", n_local);
   Levels L;
@@ -244,6 +261,7 @@ int qsb_sample_tree(qsb_ctx* ctx, const double* amps, int n_local, double* root_
 
 int qsb_sample_descend(qsb_ctx* ctx, qsb_table* t, const double* amps, int n_local, uint64_t count, const double* u,
                        int64_t* idx_out, double* cost_out) {
+  if (ctx) QSB_CUDA(cudaSetDevice(ctx->device));  // launches go to the context's GPU
   if (!ctx || !amps || (count && (!u || !idx_out))) return invalid("qsb_sample_descend: null argument");
   if (ctx->tree_n != n_local || ctx->tree_amps != amps)
     return invalid("qsb_sample_descend: no tree for this state (call qsb_sample_tree first)");

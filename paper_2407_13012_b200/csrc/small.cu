@@ -234,8 +234,11 @@ int small_run(qsb_ctx* ctx, qsb_table* t, double2* ket, int p, const double* gam
   a.mode = mode;
   a.want_value = value != nullptr;
   const size_t smem = kSmallSmem;
-  static const cudaError_t attr = cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  QSB_CUDA(attr);
+  static PerDevice<cudaError_t> attr;
+  QSB_CUDA(attr.get(ctx->device, [&] {
+    cudaError_t e = cudaSetDevice(ctx->device);
+    return e != cudaSuccess ? e : cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }));
   k_small<<<1, kST, smem, ctx->stream>>>(a);
   QSB_CHECK_LAUNCH(ctx, "small-register circuit");
   if (value || mode >= 2) {
@@ -261,6 +264,7 @@ extern "C" {
 // and phase LUT / angles, all packed into one upload.
 int qsb_small_batch(qsb_ctx* ctx, int count, qsb_table* const* tables, double* const* kets, const int* ps,
                     const double* gammas, const double* betas, int mode, double* out) {
+  if (ctx) QSB_CUDA(cudaSetDevice(ctx->device));  // launches go to the context's GPU
   if (!ctx || count < 0 || (count > 0 && (!tables || !kets || !ps || !gammas || !betas || !out)))
     return invalid("qsb_small_batch: null argument");
   if (mode < 0 || mode > 2) return invalid("qsb_small_batch: mode must be 0 (simulate), 1 (+<C>) or 2 (+gradient)");
@@ -332,9 +336,11 @@ int qsb_small_batch(qsb_ctx* ctx, int count, qsb_table* const* tables, double* c
   QSB_CUDA(cudaMemcpyAsync(d_stage, host.data(), stage_b, cudaMemcpyHostToDevice, ctx->stream));
   QSB_CUDA(cudaMemcpyAsync(d_args, args.data(), args_b, cudaMemcpyHostToDevice, ctx->stream));
   ctx->h2d_bytes += stage_b + args_b;
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(k_small_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmem);
-  QSB_CUDA(attr);
+  static PerDevice<cudaError_t> attr;
+  QSB_CUDA(attr.get(ctx->device, [&] {
+    cudaError_t e = cudaSetDevice(ctx->device);
+    return e != cudaSuccess ? e : cudaFuncSetAttribute(k_small_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmem);
+  }));
   k_small_batch<<<count, kST, kSmallSmem, ctx->stream>>>(d_args);
   QSB_CHECK_LAUNCH(ctx, "small-register batch");
   QSB_CUDA(cudaMemcpyAsync(out, d_out, out_b, cudaMemcpyDeviceToHost, ctx->stream));

@@ -893,22 +893,24 @@ template <int SH, int NV, int FORM, bool KSIN, bool FULL, int MODE = SM_PLAIN, i
 struct SweepKernel {
   static constexpr int threads = GR * (32 << shape_w(SH));
   static int grid(qsb_ctx* ctx, uint64_t ntiles, unsigned* g) {
-    // once per process (thread-safe static initialisation; one device type)
+    // once per device (function attributes are per device; thread-safe)
     struct Init {
       cudaError_t err;
       int occ;
     };
-    static const Init init = [] {
-      Init r{cudaFuncSetAttribute(k_sweep<SH, NV, FORM, KSIN, FULL, MODE, FORM2, GR, FM>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes),
-             1};
+    static PerDevice<Init> cache;
+    const Init& init = cache.get(ctx->device, [&] {
+      Init r{cudaSetDevice(ctx->device), 1};
+      if (r.err == cudaSuccess)
+        r.err = cudaFuncSetAttribute(k_sweep<SH, NV, FORM, KSIN, FULL, MODE, FORM2, GR, FM>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
       int o = 0;
       if (r.err == cudaSuccess)
         r.err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sweep<SH, NV, FORM, KSIN, FULL, MODE, FORM2, GR, FM>,
                                                               threads, kSmemBytes);
       r.occ = o < 1 ? 1 : o;
       return r;
-    }();
+    });
     QSB_CUDA(init.err);
     const uint64_t want = (uint64_t)ctx->num_sms * init.occ;
     *g = (unsigned)(ntiles < want ? ntiles : want);

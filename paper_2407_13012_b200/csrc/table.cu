@@ -194,6 +194,7 @@ int qsb_precompute_table(qsb_ctx* ctx, const double* weights, const int64_t* mas
 
 int qsb_table_create(qsb_ctx* ctx, int n, const double* weights, const int64_t* masks, uint64_t num_terms,
                      double* values, double* min_out, double* max_out, qsb_table** out) {
+  if (ctx) QSB_CUDA(cudaSetDevice(ctx->device));  // launches go to the context's GPU
   if (!ctx || !values || !out) return invalid("qsb_table_create: null argument");
   if (n < 1 || n > 62) return invalid("qsb_table_create: n=%d out of range", n);
   const uint64_t len = 1ull << n;
@@ -208,6 +209,7 @@ int qsb_table_create(qsb_ctx* ctx, int n, const double* weights, const int64_t* 
 int qsb_table_create_mapped(qsb_ctx* ctx, int n_global, int n_local, const double* weights, const int64_t* masks,
                             uint64_t num_terms, int b, int s1, int s2, uint64_t rank, double* values, double* min_out,
                             double* max_out, qsb_table** out) {
+  if (ctx) QSB_CUDA(cudaSetDevice(ctx->device));  // launches go to the context's GPU
   if (!ctx || !values || !out) return invalid("qsb_table_create_mapped: null argument");
   if (n_local < 1 || n_local > n_global || n_global > 62) return invalid("bad shard geometry %d/%d", n_local, n_global);
   const uint64_t glen = 1ull << n_global;
@@ -221,6 +223,7 @@ int qsb_table_create_mapped(qsb_ctx* ctx, int n_global, int n_local, const doubl
 }
 
 int qsb_table_wrap(qsb_ctx* ctx, int n, double* values, double* min_out, double* max_out, qsb_table** out) {
+  if (ctx) QSB_CUDA(cudaSetDevice(ctx->device));  // launches go to the context's GPU
   if (!ctx || !values || !out) return invalid("qsb_table_wrap: null argument");
   if (n < 1 || n > 62) return invalid("qsb_table_wrap: n=%d out of range", n);
   qsb_table* t = new qsb_table();

@@ -235,8 +235,16 @@ class _ShardVisit(C.Structure):
 
 
 # ---------------------------------------------------------------- exchangers
+def _ptr_array(ptrs) -> "C.Array":
+    arr = (C.c_void_p * len(ptrs))()
+    for i, p_ in enumerate(ptrs):
+        arr[i] = p_
+    return arr
+
+
 class VirtualExchanger:
-    """All G shards live in this process on one device: the all-to-all is G^2 chunk copies."""
+    """All G shards live in this process on one device: the all-to-all is one chunk
+    scatter kernel per shard (qsb_scatter_chunks) into the other shards' spares."""
 
     fused = True  # the swap is fused into the A visit's stores (shard buffers are plain device memory)
 
@@ -269,25 +277,29 @@ class VirtualExchanger:
         """element-wise sum over ranks of arrays each rank filled only where it owns the entry"""
         return arrays
 
-    def swap(self, vecs: list[DeviceArray], scratch: list[DeviceArray]) -> None:
+    def all_max(self, *vals: float) -> tuple[float, ...]:
+        return vals
+
+    def swap_vec(self, name: str, live: list[DeviceArray], spare: list[DeviceArray]) -> None:
+        """standalone qubit swap of one vector: shard r's chunk c -> shard c's chunk r"""
         G = self.G
-        chunk = len(vecs[0]) // G
-        nbytes = chunk * 16
+        chunk = len(live[0]) // G
+        dsts = _ptr_array([b.ptr for b in spare])
         for r in range(G):
-            for c in range(G):
-                call("qsb_d2d", vecs[r].dctx.handle, scratch[c].ptr + r * nbytes, vecs[r].ptr + c * nbytes, nbytes)
-        for k in range(G):  # the received data becomes the state; the old state the scratch
-            vecs[k].ptr, scratch[k].ptr = scratch[k].ptr, vecs[k].ptr
+            call("qsb_scatter_chunks", live[r].dctx.handle, live[r].ptr, chunk, G, dsts, r * chunk)
+        self.commit(name, live, spare)
 
 
 class TorchExchanger:
-    """One shard per process (torchrun).  The qubit swap is an NCCL all-to-all over
-    NVLink/NVSwitch after the A visit (default), or -- p2p=True / QSB_SHARD_P2P=1 -- fused
-    into the A visit's stores: every process opens its peers' spare buffers through CUDA
-    IPC and the sweep kernel writes each output tile straight into the shard that owns it
-    after the swap (NVLink P2P stores overlapped with the sweep; no separate pass).
-    With a gloo process group (tests: two processes on one GPU) the host-side
-    collectives run on CPU tensors."""
+    """One shard per process (torchrun).  The qubit swap is fused into the A visit's
+    stores when p2p=True / QSB_SHARD_P2P=1: every process opens its peers' spare buffers
+    through CUDA IPC and the sweep kernel writes each output tile straight into the shard
+    that owns it after the swap (NVLink P2P stores overlapped with the sweep; no separate
+    pass).  Swaps outside a fused visit (a draw after an odd number of layers, exact
+    mode, shards below 21 local qubits) then run qsb_scatter_chunks into the same peer
+    buffers.  Without P2P the swap is an NCCL all-to-all after the A visit; with a gloo
+    process group (tests: two processes on one GPU) the host-side collectives run on CPU
+    tensors and the non-P2P swap is staged through host memory."""
 
     def __init__(self, g: int, dist, device: int, p2p: bool | None = None):
         import os
@@ -313,50 +325,56 @@ class TorchExchanger:
 
     def setup(self, handle) -> None:
         """P2P mode: export this shard's live/spare buffers, open every peer's.  If any
-        rank cannot (no peer access), every rank falls back to the NCCL all-to-all."""
+        rank cannot (no peer access), every rank falls back to the all-to-all.
+
+        Every rank runs the same collectives whatever fails locally: the handles are
+        exported first (a failure only clears this rank's ok byte), exchanged in ONE
+        all_gather, opened with no collective in between, and the outcome agreed by
+        one all_reduce."""
         if not self.fused:
             return
         import torch
 
-        ok = 1
+        self._ctx = handle.ctx.device.handle
+        bufs = (("ket", handle.ket[0], handle.scratch[0]), ("bra", handle.bra[0], handle.scratch_bra[0]))
+        mine = np.zeros(257, dtype=np.uint8)
         try:
-            self._setup_p2p(handle)
+            for i, (_, b0, b1) in enumerate(bufs):
+                call("qsb_ipc_handle", self._ctx, b0.ptr, mine[128 * i:128 * i + 64].ctypes.data)
+                call("qsb_ipc_handle", self._ctx, b1.ptr, mine[128 * i + 64:128 * i + 128].ctypes.data)
+            mine[256] = 1
         except Exception:  # noqa: BLE001 -- decided collectively below
-            ok = 0
+            mine[256] = 0
+        t = torch.as_tensor(mine, device=self._tdev())
+        out = [torch.empty_like(t) for _ in range(self.G)]
+        self.dist.all_gather(out, t)
+        handles = [np.ascontiguousarray(o.cpu().numpy()) for o in out]
+        ok = int(all(h[256] == 1 for h in handles))
+        if ok:
+            try:
+                for i, (name, b0, b1) in enumerate(bufs):
+                    ptrs = []
+                    for r in range(self.G):
+                        if r == self.rank:
+                            ptrs.append([b0.ptr, b1.ptr])
+                            continue
+                        pp = []
+                        for off in (128 * i, 128 * i + 64):
+                            p_ = C.c_void_p()
+                            call("qsb_ipc_open", self._ctx, handles[r][off:off + 64].ctypes.data, C.byref(p_))
+                            pp.append(p_.value)
+                            self._opened.append(p_.value)
+                        ptrs.append(pp)
+                    self._peers[name] = ptrs
+                    self._parity[name] = 0
+            except Exception:  # noqa: BLE001
+                ok = 0
         flag = torch.tensor([ok], dtype=torch.int32, device=self._tdev())
         self.dist.all_reduce(flag, op=self.dist.ReduceOp.MIN)
         if int(flag.item()) == 0:
             self.close()
             self._peers, self._parity = {}, {}
             self.fused = False
-
-    def _setup_p2p(self, handle) -> None:
-        import torch
-
-        self._ctx = handle.ctx.device.handle
-        for name, (b0, b1) in (("ket", (handle.ket[0], handle.scratch[0])),
-                               ("bra", (handle.bra[0], handle.scratch_bra[0]))):
-            mine = np.zeros(128, dtype=np.uint8)
-            call("qsb_ipc_handle", self._ctx, b0.ptr, mine[:64].ctypes.data)
-            call("qsb_ipc_handle", self._ctx, b1.ptr, mine[64:].ctypes.data)
-            t = torch.as_tensor(mine, device=self._tdev())
-            out = [torch.empty_like(t) for _ in range(self.G)]
-            self.dist.all_gather(out, t)
-            ptrs = []
-            for r in range(self.G):
-                if r == self.rank:
-                    ptrs.append([b0.ptr, b1.ptr])
-                    continue
-                hb = np.ascontiguousarray(out[r].cpu().numpy())
-                pp = []
-                for off in (0, 64):
-                    p_ = C.c_void_p()
-                    call("qsb_ipc_open", self._ctx, hb[off:off + 64].ctypes.data, C.byref(p_))
-                    pp.append(p_.value)
-                    self._opened.append(p_.value)
-                ptrs.append(pp)
-            self._peers[name] = ptrs
-            self._parity[name] = 0
 
     def targets(self, name: str, spare: list[DeviceArray]) -> list[int]:
         par = self._parity[name]
@@ -405,17 +423,36 @@ class TorchExchanger:
             res.append(t.cpu().numpy())
         return tuple(res)
 
-    def swap(self, vecs: list[DeviceArray], scratch: list[DeviceArray]) -> None:
+    def all_max(self, *vals: float) -> tuple[float, ...]:
         import torch
 
+        t = torch.tensor(list(vals), dtype=torch.float64, device=self._tdev())
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return tuple(float(x) for x in t.tolist())
+
+    def swap_vec(self, name: str, live: list[DeviceArray], spare: list[DeviceArray]) -> None:
+        """Standalone qubit swap of one vector (see the class doc): P2P chunk scatter into
+        the peers' spare buffers, else an all-to-all (NCCL; host-staged over gloo)."""
+        import torch
+
+        v, s = live[0], spare[0]
+        chunk = len(v) // self.G
         if self.fused:
-            raise ContractViolation("the P2P exchanger swaps inside the sweeps (fast-mode window chain only)")
-        v, s = vecs[0], scratch[0]
-        v.dctx.sync()  # our stream -> NCCL's stream
-        src = torch.as_tensor(_CudaView(v), device=f"cuda:{self.device}").view(self.G, -1)
-        dst = torch.as_tensor(_CudaView(s), device=f"cuda:{self.device}").view(self.G, -1)
-        self.dist.all_to_all_single(dst, src)
-        torch.cuda.synchronize(self.device)
+            call("qsb_scatter_chunks", self._ctx, v.ptr, chunk, self.G, _ptr_array(self.targets(name, spare)),
+                 self.rank * chunk)
+            self.commit(name, live, spare)
+            return
+        if self.cpu:  # gloo stand-in: D2H, all-to-all of host tensors, H2D into the spare
+            host = torch.from_numpy(v.to_host().view(np.float64)).view(self.G, -1)
+            recv = torch.empty_like(host)
+            self.dist.all_to_all_single(recv, host)
+            s.from_host(recv.numpy().reshape(-1).view(np.complex128))
+        else:
+            v.dctx.sync()  # our stream -> NCCL's stream
+            src = torch.as_tensor(_CudaView(v), device=f"cuda:{self.device}").view(self.G, -1)
+            dst = torch.as_tensor(_CudaView(s), device=f"cuda:{self.device}").view(self.G, -1)
+            self.dist.all_to_all_single(dst, src)
+            torch.cuda.synchronize(self.device)
         v.ptr, s.ptr = s.ptr, v.ptr
 
 
@@ -436,37 +473,36 @@ class _CudaView:
 # ---------------------------------------------------------------- sharded handle
 class ShardedHandle:
     """A polynomial's statevector split over 2^g shards (this process holds
-    `exchanger.ranks`), with cost tables for both layouts."""
+    `exchanger.ranks`), with cost tables for both layouts.
+
+    Per-GPU memory (N_l = 2^(n-g) amplitudes per shard): ket, bra and one spare per
+    vector for the qubit swap (4 x 16 N_l B) plus each layout's table -- the 1-2 B/amp
+    compact index when the table is integral with < 65536 distinct values (the fp64
+    copy is built, compacted and freed one layout at a time), else fp64 (8 B/amp).
+    n = 34 on 8 GPUs (N_l = 2^31, MaxCut u8 index): 128 GiB + 2 x 2 GiB + the
+    sampler's 1 GiB level scratch, ~134 GiB of the B200's ~178 GiB (DESIGN.md (e))."""
 
     def __init__(self, poly: costpoly.Polynomial, g: int, exchanger, device: int | None = None):
         n = poly.n
         if g < 1:
             raise ContractViolation("sharding needs g >= 1 (use create_handle for one GPU)")
+        if g > 3:
+            raise ContractViolation(f"at most 8 shards (g <= 3), got g={g}")
         if n - g < 12:
             raise ContractViolation(f"shards need >= 12 local qubits (n={n}, g={g})")
         self.n, self.g, self.n_l = n, g, n - g
         self.poly = poly
         self.ex = exchanger
-        if device is not None:
-            import os
-
-            os.environ["QAOA_DEVICE"] = str(device)
-        self.ctx = backend.create_context("b200")
+        self.ctx = backend.create_context("b200", device)
         dctx = self.ctx.device
         N_l = 1 << self.n_l
         self.ranks = list(exchanger.ranks)
-        self.ket = [DeviceArray(dctx, N_l, np.complex128) for _ in self.ranks]
-        self.bra = [DeviceArray(dctx, N_l, np.complex128) for _ in self.ranks]
-        self.scratch = [DeviceArray(dctx, N_l, np.complex128) for _ in self.ranks]
-        # the fused swap of a bra/ket visit needs a second spare buffer (allocated lazily,
-        # up front for P2P so it can be exported)
-        self.scratch_bra = None
-        if exchanger.fused and not isinstance(exchanger, VirtualExchanger):
-            self.scratch_bra = [DeviceArray(dctx, N_l, np.complex128) for _ in self.ranks]
+        # tables first (their fp64 build buffers are transient), then the statevectors
         w = np.ascontiguousarray(poly.weights, dtype=np.float64)
         m = np.ascontiguousarray(poly.masks, dtype=np.int64)
         self.tables = [[None] * len(self.ranks), [None] * len(self.ranks)]
         lo, hi = np.inf, -np.inf
+        self.table_bytes = 0
         for layout in (0, 1):
             for k, r in enumerate(self.ranks):
                 vals = DeviceArray(dctx, N_l, np.float64)
@@ -475,20 +511,43 @@ class ShardedHandle:
                 call("qsb_table_create_mapped", dctx.handle, n, self.n_l, w.ctypes.data, m.ctypes.data, w.shape[0],
                      b, s1, s2, rank, vals.ptr, C.byref(mn), C.byref(mx), C.byref(ptr))
                 b200._attach(vals, ptr)
+                if vals.table.kind != 0:  # the sweeps and the sampler read the compact index only
+                    call("qsb_table_detach_values", vals.table.ptr)
+                    vals.free()
+                    self.table_bytes += N_l * vals.table.kind
+                else:
+                    self.table_bytes += 8 * N_l
                 self.tables[layout][k] = vals
                 lo, hi = min(lo, mn.value), max(hi, mx.value)
         self.min_value, self.max_value = self._minmax(lo, hi)
+        self.ket = [DeviceArray(dctx, N_l, np.complex128) for _ in self.ranks]
+        self.bra = [DeviceArray(dctx, N_l, np.complex128) for _ in self.ranks]
+        self.scratch = [DeviceArray(dctx, N_l, np.complex128) for _ in self.ranks]
+        # a fused swap of a bra/ket visit needs a second spare (up front for P2P, whose
+        # buffers are exported once; lazily for virtual shards)
+        self.scratch_bra = None
+        if exchanger.fused and not isinstance(exchanger, VirtualExchanger):
+            self.scratch_bra = [DeviceArray(dctx, N_l, np.complex128) for _ in self.ranks]
         self.layout = 0
+        self._plus_pending = False  # the ket is |+> by contract but not written (after a gradient)
         exchanger.setup(self)
 
     def _minmax(self, lo: float, hi: float) -> tuple[float, float]:
-        if isinstance(self.ex, VirtualExchanger):
-            return lo, hi
-        import torch
+        neg_lo, hi = self.ex.all_max(-lo, hi)
+        return -neg_lo, hi
 
-        t = torch.tensor([-lo, hi], dtype=torch.float64, device=self.ex._tdev())
-        self.ex.dist.all_reduce(t, op=self.ex.dist.ReduceOp.MAX)
-        return -float(t[0]), float(t[1])
+    def _spare(self, name: str) -> list[DeviceArray]:
+        if name == "ket":
+            return self.scratch
+        if self.scratch_bra is not None and not isinstance(self.ex, VirtualExchanger):
+            return self.scratch_bra  # P2P: the exported bra spares
+        return self.scratch
+
+    def _swap(self, nv: int) -> None:
+        """standalone qubit swap (layout A <-> B) of the ket (and the bra)"""
+        self.ex.swap_vec("ket", self.ket, self._spare("ket"))
+        if nv == 2:
+            self.ex.swap_vec("bra", self.bra, self._spare("bra"))
 
     # -- execution
     def _run(self, steps, exact: bool) -> list[np.ndarray]:
@@ -496,9 +555,7 @@ class ShardedHandle:
         sums_per_step = []
         for st in steps:
             if isinstance(st, Swap):
-                self.ex.swap(self.ket, self.scratch)
-                if st.nv == 2:
-                    self.ex.swap(self.bra, self.scratch)
+                self._swap(st.nv)
                 layout ^= 1
                 sums_per_step.append(None)
                 continue
@@ -556,9 +613,7 @@ class ShardedHandle:
                     if v.nv == 2:
                         self.ex.commit("bra", self.bra, self.scratch_bra)
                 else:
-                    self.ex.swap(self.ket, self.scratch)
-                    if v.nv == 2:
-                        self.ex.swap(self.bra, self.scratch)
+                    self._swap(v.nv)
                 layout ^= 1
         stacked = [np.concatenate([pv[k] for pv in per_visit]) for k in range(len(self.ranks))]
         total = self.ex.combine(stacked)
@@ -568,17 +623,21 @@ class ShardedHandle:
     def value_and_grad(self, params: circuit.QaoaParams, exact: bool = False):
         if params.p < 1:
             raise ContractViolation("gradient needs depth p >= 1")
+        self._plus_pending = False
         if self._use_chain(exact):
             visits = chain_program(self.n, self.g, params.gammas, params.betas, True, True)
             value, dg, db = collect_chain(visits, self._run_chain(visits), params.p)
-            return self._clamp(value), dg, db
-        steps = program(self.n, self.g, params.gammas, params.betas, True, True)
-        value, dg, db = collect(steps, self._run(steps, exact), params.p)
+        else:
+            steps = program(self.n, self.g, params.gammas, params.betas, True, True)
+            value, dg, db = collect(steps, self._run(steps, exact), params.p)
+        # the walk's last sweep only contracts: the ket is |+> by contract (adjoint.py:39-42)
+        self._plus_pending = True
         return self._clamp(value), dg, db
 
     def expectation(self, params: circuit.QaoaParams, exact: bool = False) -> float:
         if params.p < 1:
             raise ContractViolation("sharded expectation needs p >= 1")
+        self._plus_pending = False
         if self._use_chain(exact):
             visits = chain_program(self.n, self.g, params.gammas, params.betas, True, False)
             value, _, _ = collect_chain(visits, self._run_chain(visits), params.p)
@@ -590,31 +649,52 @@ class ShardedHandle:
     def _clamp(self, v: float) -> float:
         return min(max(v, self.min_value), self.max_value)
 
+    def _materialize(self) -> None:
+        """write a pending |+> (1/sqrt(2^n) on every shard, layout-independent)"""
+        if self._plus_pending:
+            amp = 1.0 / np.sqrt(float(1 << self.n))
+            for k in range(len(self.ranks)):
+                call("qsb_fill_const", self.ctx.device.handle, self.ket[k].ptr, 1 << self.n_l, amp, 0.0)
+            self.layout = 0
+            self._plus_pending = False
+
     def gather_state(self) -> np.ndarray:
         """Full statevector in global index order (virtual shards, tests)."""
         if not isinstance(self.ex, VirtualExchanger):
             raise ContractViolation("gather_state needs all shards in this process")
+        self._materialize()
         out = np.empty(1 << self.n, dtype=np.complex128)
         i = np.arange(1 << self.n_l, dtype=np.int64)
         for k, r in enumerate(self.ranks):
             out[global_index(self.layout, self.n, self.g, r, i)] = self.ket[k].to_host()
         return out
 
+    def local_state(self) -> tuple[np.ndarray, np.ndarray]:
+        """(global indices, amplitudes) of this process's shard(s) in the current layout."""
+        self._materialize()
+        i = np.arange(1 << self.n_l, dtype=np.int64)
+        idx = np.concatenate([global_index(self.layout, self.n, self.g, r, i) for r in self.ranks])
+        amps = np.concatenate([self.ket[k].to_host() for k in range(len(self.ranks))])
+        return idx, amps
+
     def draw(self, shots: int, seed: int) -> "sampling.SampleSet":
         """Sample the sharded state (sampling.draw semantics: indices in draw order, the
         reference's probability-tree association and splitmix64 uniforms, so the
         indices equal those of the unsharded state's draw).
 
-        Shards build their subtrees on their GPUs (qsb_sample_tree); the G roots are
-        gathered and combined pairwise exactly like the reference's upper tree levels;
-        every rank draws u_s = U(seed, s) * total and descends those g levels (identical
-        arithmetic everywhere), then each shard descends its own shots on the device
+        The state first returns to layout A (rank bits = top index bits) with a
+        standalone swap when an odd number of swaps preceded.  Shards build their
+        subtrees on their GPUs (qsb_sample_tree); the G roots are gathered and combined
+        pairwise exactly like the reference's upper tree levels; every rank draws
+        u_s = U(seed, s) * total and descends those g levels (identical arithmetic
+        everywhere), then each shard descends its own shots on the device
         (qsb_sample_descend) and the per-shot results are summed over ranks (one owner
         per shot)."""
         if shots < 1:
             raise ContractViolation(f"shots must be >= 1, got {shots}")
+        self._materialize()
         if self.layout != 0:  # back to layout A: the rank bits are the top index bits
-            self.ex.swap(self.ket, self.scratch)
+            self._swap(1)
             self.layout = 0
         h = self.ctx.device.handle
         local = []
@@ -656,11 +736,18 @@ class ShardedHandle:
         return sampling.SampleSet(shots=shots, seed=seed, indices=idx, costs=cost)
 
     def simulate(self, params: circuit.QaoaParams, exact: bool = False) -> None:
+        self._plus_pending = False
         if self._use_chain(exact) and params.p >= 1:
             self._run_chain(chain_program(self.n, self.g, params.gammas, params.betas, False, False))
             return
         steps = program(self.n, self.g, params.gammas, params.betas, False, False)
         self._run(steps, exact)
+
+    def memory_bytes(self) -> int:
+        """device bytes this process holds for the handle (statevectors + tables)"""
+        N_l = 1 << self.n_l
+        nvec = 3 + (1 if self.scratch_bra is not None else 0)
+        return len(self.ranks) * nvec * 16 * N_l + self.table_bytes
 
     def close(self) -> None:
         if hasattr(self.ex, "close"):

@@ -29,8 +29,8 @@ def _device_index() -> int:
     return 0
 
 
-def open_device() -> DeviceContext:
-    return DeviceContext(_device_index())
+def open_device(device: int | None = None) -> DeviceContext:
+    return DeviceContext(_device_index() if device is None else int(device))
 
 
 def empty(dctx: DeviceContext, length: int, dtype) -> DeviceArray:

@@ -160,3 +160,104 @@ def test_all_to_all_over_gloo_is_the_layout_swap():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}
+
+
+class _HostArr:
+    """host stand-in for a DeviceArray: memory addressed by .ptr (so pointer swaps
+    behave like the device buffers')"""
+
+    store: dict = {}
+
+    def __init__(self, values):
+        self.ptr = len(_HostArr.store) + 1000
+        _HostArr.store[self.ptr] = np.array(values, dtype=np.complex128)
+
+    def __len__(self):
+        return len(_HostArr.store[self.ptr])
+
+    def to_host(self):
+        return _HostArr.store[self.ptr].copy()
+
+    def from_host(self, values):
+        _HostArr.store[self.ptr][:] = values
+
+
+def _staged_swap_worker(rank, world, port, n, g, q):
+    import torch.distributed as tdist
+
+    tdist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        psi = (np.arange(1 << n, dtype=np.float64) * 1.5 + 0.25) * (1 - 0.5j)
+        i = np.arange(1 << (n - g))
+        ex = dist.TorchExchanger(g, tdist, 0, p2p=False)
+        live = [_HostArr(psi[dist.global_index(0, n, g, rank, i)])]
+        spare = [_HostArr(np.zeros(1 << (n - g)))]
+        ex.swap_vec("ket", live, spare)  # the non-P2P branch over gloo: staged through the host
+        ok = np.array_equal(live[0].to_host(), psi[dist.global_index(1, n, g, rank, i)])
+        ex.swap_vec("ket", live, spare)  # and back
+        ok = ok and np.array_equal(live[0].to_host(), psi[dist.global_index(0, n, g, rank, i)])
+    finally:
+        tdist.destroy_process_group()
+    q.put((rank, bool(ok)))
+
+
+def _p2p_setup_worker(rank, world, port, q):
+    """rank 0 exports its IPC handles, rank 1 fails to: both must still run the same
+    collectives and agree to fall back (no mismatched all_gather / all_reduce hang)"""
+    import torch.distributed as tdist
+
+    from paper_2407_13012_b200 import _lib
+
+    tdist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        def fake_call(name, *args):
+            if rank == 1 or name != "qsb_ipc_handle":
+                raise _lib.ContractViolation(f"{name}: no peer access on rank {rank}")
+
+        dist.call = fake_call
+
+        class _Dev:
+            handle = None
+
+        class _Ctx:
+            device = _Dev()
+
+        class _H:
+            ctx = _Ctx()
+            ket = [_HostArr(np.zeros(4))]
+            scratch = [_HostArr(np.zeros(4))]
+            bra = [_HostArr(np.zeros(4))]
+            scratch_bra = [_HostArr(np.zeros(4))]
+
+        ex = dist.TorchExchanger(1, tdist, 0, p2p=True)
+        ex.setup(_H())
+        q.put((rank, ex.fused))
+    finally:
+        tdist.destroy_process_group()
+
+
+def _spawn(target, args_of_rank, world=2):
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=target, args=(r, world, port, *args_of_rank(r), q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    return res
+
+
+def test_torch_exchanger_staged_swap_over_gloo():
+    """TorchExchanger.swap_vec without P2P on a gloo group: D2H, all_to_all_single of
+    host tensors, H2D into the spare, pointer swap -- layout A <-> B exactly"""
+    assert _spawn(_staged_swap_worker, lambda r: (9, 1)) == {0: True, 1: True}
+
+
+def test_p2p_setup_failure_on_one_rank_falls_back_everywhere():
+    assert _spawn(_p2p_setup_worker, lambda r: ()) == {0: False, 1: False}

@@ -115,31 +115,53 @@ def test_sharded_window_chain(n, g, p, monkeypatch):
     assert rel_err(st1, st0) <= 1e-12
 
 
-def test_two_process_p2p_swap(tmp_path):
-    """Two processes, one shard each, the qubit swap fused into the A visit's stores
-    through CUDA IPC (QSB_SHARD_P2P path of dist.TorchExchanger) -- both on the one GPU
-    here; equals the single-process virtual-shard run."""
+@pytest.mark.parametrize("mode", ["p2p", "staged"])
+@pytest.mark.parametrize("n,p", [(22, 3), (16, 3)])
+def test_two_process_sharded(tmp_path, mode, n, p):
+    """Two processes, one shard each (both on the one GPU here), for both transports
+    of dist.TorchExchanger: "p2p" (qubit swap fused into the A visit's stores through
+    CUDA IPC; standalone swaps by the peer chunk scatter) and "staged" (the all-to-all
+    branch, host-staged over gloo).  n=22: the window chain (n_l = 21); n=16: the
+    per-position schedule (n_l < 21: every swap standalone).  Fast and exact
+    value_and_grad, a draw after an odd number of layers (layout B -> swap back) and a
+    draw after a gradient (ket |+> by contract) equal the single-process virtual-shard
+    run and the CPU oracle."""
     import os
     import subprocess
     import sys
 
-    n, p = 22, 2
     out = tmp_path / "res.npz"
-    env = dict(os.environ, QSB_SHARD_P2P="1")
+    port = 29531 + (n % 7) * 2 + (mode == "p2p")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", "--master-port=29531",
-           os.path.join(os.path.dirname(__file__), "mp_shard_worker.py"), str(out), str(n), str(p)]
-    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+           "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.join(os.path.dirname(__file__), "mp_shard_worker.py"), str(out), str(n), str(p), mode]
+    res = subprocess.run(cmd, env=dict(os.environ), capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stderr[-3000:]
     got = np.load(out)
+    assert int(got["fused"]) == (1 if mode == "p2p" else 0)
+    assert int(got["layout"]) == p % 2  # one swap per layer: odd p ends in layout B
     poly = random_instance(70 + n, n)
     params = random_params(n + 3, p)
     sh = dist.ShardedHandle(poly, 1, dist.VirtualExchanger(1))
     v, dg, db = sh.value_and_grad(params)
+    vx, dgx, dbx = sh.value_and_grad(params, exact=True)
+    sh.simulate(params)
+    state = sh.gather_state()
     sh.close()
     assert abs(float(got["v"]) - v) <= 1e-12 * max(1.0, abs(v))
     assert abs(float(got["e"]) - v) <= 1e-11 * max(1.0, abs(v))
     assert rel_err(np.concatenate([got["dg"], got["db"]]), np.concatenate([dg, db])) <= 1e-12
+    assert float(got["vx"]) == vx
+    assert np.array_equal(got["dgx"], dgx) and np.array_equal(got["dbx"], dbx)
+    table = oracle.precompute_table(poly.weights, poly.masks, n)
+    e, wdg, wdb = oracle.value_and_grad(table, n, params.gammas, params.betas)
+    assert abs(v - e) <= 1e-10 * max(1.0, abs(e))
+    assert rel_err(np.concatenate([dgx, dbx]), np.concatenate([wdg, wdb])) <= 1e-10
+    idx, cost = oracle.sample(state, table, 4000, 11)
+    assert np.array_equal(got["idx"], idx) and np.array_equal(got["cost"], cost)
+    plus = np.full(1 << n, 1.0 / np.sqrt(float(1 << n)), dtype=np.complex128)
+    gidx, gcost = oracle.sample(plus, table, 3000, 5)
+    assert np.array_equal(got["gidx"], gidx) and np.array_equal(got["gcost"], gcost)
 
 
 def test_sharded_chain_float_table_and_sampling():
