@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--params", choices=["ramp", "random"], default="ramp")
     ap.add_argument("--shots", type=int, default=1_000_000)
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent n=30 replicas instead of sharding")
+    ap.add_argument("--no-c4", action="store_true", help="N = 2/4: skip the config-4 lines (C5 ladder only)")
+    ap.add_argument("--calibrate-cpu", default=None,
+                    help="comma list of n: time the CPU baseline's E+grad at each size and exit (scaling check)")
     return ap.parse_args()
 
 
@@ -293,86 +296,196 @@ def load_traffic() -> dict:
     return json.loads(p.read_text()) if p.exists() else {}
 
 
-def run_sharded(args, rank: int, world: int, dist) -> None:
-    """N > 1: one n-qubit state sharded over all N GPUs (top log2 N qubits global),
-    index-bit swaps by NCCL all-to-all.  Weak scaling: n = 30 + log2 N keeps 2^30
-    amplitudes per GPU (unless --n is given)."""
+def qubo_polynomial(n: int, seed: int):
+    """C4 dense QUBO: n linear + n(n-1)/2 pair terms, weights (U - 0.5) * 8 from
+    rng.Stream(seed) (float weights -> fp64 table + device sincos)"""
+    import paper_2407_13012_b200 as qs
+    from paper_2407_13012_b200 import rng
+
+    st = rng.Stream(seed)
+    terms = [((st.next_uniform() - 0.5) * 8.0, 1 << i) for i in range(n)]
+    for i in range(n):
+        for j in range(i + 1, n):
+            terms.append(((st.next_uniform() - 0.5) * 8.0, (1 << i) | (1 << j)))
+    return qs.Polynomial(n, terms)
+
+
+def weighted_maxcut(n: int, seed: int):
+    """C4 weighted MaxCut on K_n, integer weights 1 + floor(8U) (bit-exact table, u16 index)"""
+    import paper_2407_13012_b200 as qs
+    from paper_2407_13012_b200 import rng
+
+    st = rng.Stream(seed)
+    edges = [(u, v, float(1 + int(8 * st.next_uniform()))) for u in range(n) for v in range(u + 1, n)]
+    return qs.maxcut_polynomial(qs.Graph(n, edges))
+
+
+def _sharded_eval(qdist, poly, params, g: int, dist, local: int, steps: int, warmup: int, peak_gbs: float,
+                  clocks: bool = False) -> dict:
+    """E+grad of one sharded problem: ShardedHandle over all ranks, `warmup` untimed then
+    `steps` timed value_and_grad calls.  Device time from CUDA events on the context
+    stream (max over ranks); wall clock around the public call (host params in, host
+    value / gradient out) for e2e; per-kind sweep bytes and time from the live
+    profiler; NVLink bytes of the qubit swaps from the schedule."""
     import torch
 
+    ex = qdist.TorchExchanger(g, dist, local)
+    t0 = time.perf_counter()
+    sh = qdist.ShardedHandle(poly, g, ex, device=local)
+    sh.ctx.synchronize()
+    setup_s = time.perf_counter() - t0
+    dev = sh.ctx.device
+    for _ in range(warmup):
+        sh.value_and_grad(params)
+    dev.sync()
+    dist.barrier()
+    launches0 = dev.launches()
+    with (ClockSampler(local) if clocks else _NullCtx()) as clk:
+        dev.timer_start()
+        dev.prof_begin()
+        w0 = time.perf_counter()
+        for _ in range(steps):
+            value, dg, db = sh.value_and_grad(params)
+        w1 = time.perf_counter()
+        prof = dev.prof_end()
+        ms = dev.timer_stop()
+        dev.sync()
+    launches = dev.launches() - launches0
+    wall_ms = (w1 - w0) * 1e3
+    sweep_ms = sum(v[1] for v in prof.values())
+    sweep_bytes = sum(v[2] for v in prof.values())
+    ms, wall_ms = ex.all_max(ms, wall_ms)
+    n_l = sh.n_l
+    G = 1 << g
+    # one swap per layer of the forward walk (ket) and of the backward walk (bra + ket)
+    nvlink_per_step = params.p * 3 * (1 - 1 / G) * 16 * (1 << n_l)
+    mem = sh.memory_bytes()
+    out = {
+        "n": sh.n, "p": params.p, "g": g, "n_local": n_l, "terms": poly.num_terms,
+        "table": "compact" if sh.table_bytes < 8 * (1 << n_l) * 2 else "fp64",
+        "transport": "NVLink P2P stores fused into the A visit (CUDA IPC)" if ex.fused else
+                     ("NCCL all_to_all_single" if not ex.cpu else "gloo, host-staged"),
+        "ms_per_step": ms / steps, "wall_ms_per_step": wall_ms / steps, "setup_s": setup_s,
+        "gpu_launches_per_step": launches / steps, "expectation": value,
+        "grad_norm_inf": float(max(np.abs(dg).max(), np.abs(db).max())),
+        "memory_gib_per_gpu": mem / 2**30,
+        "per_gpu_hbm_bytes_per_step": sweep_bytes / steps,
+        "nvlink_bytes_per_step_per_direction": nvlink_per_step,
+        "kernels": {k: {"launches_per_step": v[0] / steps, "ms_per_step": v[1] / steps,
+                        "gbs": v[2] / (v[1] * 1e-3) / 1e9, "frac": v[2] / (v[1] * 1e-3) / 1e9 / peak_gbs}
+                    for k, v in prof.items() if v[0] > 0},
+        "sweeps_share_of_step": sweep_ms / (ms if ms > 0 else 1.0),
+        "clocks": clk.summary() if clocks else None,
+    }
+    hbm_s = out["per_gpu_hbm_bytes_per_step"] / (peak_gbs * 1e9)
+    nvl_s = nvlink_per_step / 900e9
+    out["roofline"] = {
+        "bound": "hbm" if hbm_s >= nvl_s else "nvlink",
+        "achieved": out["per_gpu_hbm_bytes_per_step"] / (out["ms_per_step"] * 1e-3) / 1e9,
+        "peak": peak_gbs, "unit": "GB/s",
+        "frac": out["per_gpu_hbm_bytes_per_step"] / (out["ms_per_step"] * 1e-3) / 1e9 / peak_gbs,
+        "traffic": None,
+        "step_model_ms": 1e3 * max(hbm_s, nvl_s),
+        "frac_of_step_model": 1e3 * max(hbm_s, nvl_s) / out["ms_per_step"],
+        "how": "per-GPU algorithmic HBM bytes of the step's sweeps (live profiler) / device ms per step; "
+               "model = max(HBM bytes / peak, NVLink bytes per direction / 900 GB/s)",
+    }
+    sh.close()
+    torch.cuda.synchronize(local) if torch.cuda.is_available() else None
+    return out
+
+
+class _NullCtx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+def run_sharded(args, rank: int, world: int, dist) -> None:
+    """N > 1 (torchrun, one process per GPU): BASELINE.json config 5's weak-scaling ladder
+    -- MaxCut regular graph, p=6, 2^31 amplitudes per GPU, n = 31 + log2 N (n=34 on 8
+    GPUs, the headline; odd n uses a 4-regular graph) -- and, at N = 2 and 4, config 4:
+    n=32, p=8, weighted MaxCut on K32 and a dense QUBO.  The statevector is sharded on
+    the top log2 N qubits; the qubit swap is fused into the sweeps' stores over NVLink
+    (CUDA IPC peer buffers; QSB_SHARD_P2P=0: NCCL all-to-all).  value = n=30-equivalent
+    E+grad evaluations/s (steps x 2^(n-30) / max-over-ranks device time).
+    QSB_BENCH_SHARD_NL=k overrides the local qubits (same-GPU smoke runs: several
+    processes on one GPU need small shards)."""
     import paper_2407_13012_b200 as qs
     from paper_2407_13012_b200 import dist as qdist
 
     g = world.bit_length() - 1
-    if 1 << g != world:
-        raise SystemExit("sharded bench needs a power-of-two GPU count")
+    if 1 << g != world or g > 3:
+        raise SystemExit("sharded bench needs 2, 4 or 8 GPUs")
     local = int(os.environ.get("LOCAL_RANK_DEVICE", os.environ.get("LOCAL_RANK", "0")))
-    tdev = "cpu" if dist.get_backend() == "gloo" else f"cuda:{local}"
-    n = args.n if args.n != N_QUBITS else N_QUBITS + g
-    poly, params = workload(n, args.p, args.params)
-    # the qubit swap fused into the sweeps' stores over NVLink (CUDA IPC peer buffers);
-    # QSB_SHARD_P2P=0 falls back to an NCCL all-to-all after the A visit
+    nl_over = os.environ.get("QSB_BENCH_SHARD_NL")
+    n_l = int(nl_over) if nl_over else 31
+    n = args.n if args.n != N_QUBITS else n_l + g
     os.environ.setdefault("QSB_SHARD_P2P", "1")
-    ex = qdist.TorchExchanger(g, dist, local)
-    t0 = time.perf_counter()
-    sh = qdist.ShardedHandle(poly, g, ex, device=local)
-    torch.cuda.synchronize(local)
-    setup_s = time.perf_counter() - t0
-    dev = sh.ctx.device
-    for _ in range(args.warmup):
-        sh.value_and_grad(params)
+    os.environ.setdefault("QAOA_MAX_QUBITS", "62")
+    peaks = load_peaks()
+    poly, params = workload(n, args.p, args.params)
+    main = _sharded_eval(qdist, poly, params, g, dist, local, args.steps, args.warmup, peaks["hbm_gbs"], clocks=True)
+    c4 = {}
+    if world in (2, 4) and not args.no_c4:
+        n4 = 32 if not nl_over else n_l + g
+        for name, mk in (("weighted_maxcut_K32", weighted_maxcut), ("dense_qubo", qubo_polynomial)):
+            c4[name] = _sharded_eval(qdist, mk(n4, 1), qs.linear_ramp_params(8), g, dist, local,
+                                     max(2, min(args.steps, 3)), 1, peaks["hbm_gbs"])
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        n_s = min(n, sample_size(n, args.p, 15.0))
+        smp = oracle_e_plus_grad(n_s, args.p, args.params)
+        sec = scaled(smp, n, args.p)
+        cpu = {"value": 2.0 ** (n - N_QUBITS) / sec, "unit": UNIT, "cores": smp["threads"], "kind": "port",
+               "sample": f"EXTRAPOLATED: one measured end-to-end E+grad (oracle port) at n={n_s}, p={args.p}: "
+                         f"{smp['seconds']:.2f} s, scaled x2^{n - n_s} x passes({n})/passes({n_s}) to n={n} "
+                         f"(a full n={n} CPU run needs {(16 * 2 + 8) * 2 ** (n - 30):.0f} GiB of host RAM)"}
     dist.barrier()
-    dev.sync()
-    torch.cuda.synchronize(local)
-    launches0 = dev.launches()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        ev0.record()
-        for _ in range(args.steps):
-            value, dg, db = sh.value_and_grad(params)
-        dev.sync()
-        torch.cuda.synchronize(local)
-        ev1.record()
-        ev1.synchronize()
-    ms = ev0.elapsed_time(ev1)
-    launches = dev.launches() - launches0
-    t = torch.tensor([ms], dtype=torch.float64, device=tdev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    if rank == 0:
-        work = 2.0 ** (n - N_QUBITS)  # n=30-equivalent evaluations per step
-        line = {
-            "metric": METRIC,
-            "value": args.steps * work / (ms / 1e3),
-            "unit": UNIT,
-            "n_gpus": world,
-            "steps": args.steps,
-            "warmup": args.warmup,
-            "ms_per_step": ms / args.steps,
-            "higher_is_better": True,
-            "scaling": "weak",
-            "vs_baseline": None,
-            "dtype": "c128",
-            "data": "synthetic (reference graph generator, seed 1)",
-            "config": {
-                "workload": f"sharded MaxCut regular graph n={n} (random_regular(n,{3 if n % 2 == 0 else 4},seed=1)) "
-                            f"over {world} GPUs (top {g} qubits global; index-bit swap "
-                            f"{'fused into the sweep stores, NVLink P2P' if ex.fused else 'by NCCL all-to-all'}), "
-                            f"p={args.p}; one step = expectation + full adjoint gradient (window chain)",
-                "n": n, "p": args.p, "global_batch": 1, "parallelism": f"statevector sharded x{world}",
-                "value_definition": f"steps * 2^(n-30) / time: n=30-equivalent E+grad evaluations/s",
-                "l2": "no flush: 16 GiB per-GPU shard >> 126 MB L2",
-            },
-            "expectation": value,
-            "grad_norm_inf": float(max(np.abs(dg).max(), np.abs(db).max())),
-            "setup_s": setup_s,
-            "gpu_launches": launches,
-            "e2e": {"value": args.steps * work / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 16 * args.p,
-                    "d2h_bytes_per_step": 0,
-                    "how": "host params in, host E/gradient out through dist.ShardedHandle (device-event timed)"},
-            "clocks": clk.summary(),
-        }
-        print(json.dumps(line), flush=True)
-    sh.close()
+    if rank != 0:
+        return
+    work = 2.0 ** (n - N_QUBITS)  # n=30-equivalent evaluations per step
+    ms = main["ms_per_step"]
+    line = {
+        "metric": METRIC,
+        "value": work / (ms / 1e3),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c128",
+        "data": "synthetic (reference graph generator, seed 1)",
+        "config": {
+            "workload": f"C5 ladder: sharded MaxCut {3 if n % 2 == 0 else 4}-regular n={n} "
+                        f"(random_regular(n,{3 if n % 2 == 0 else 4},seed=1)) over {world} GPUs "
+                        f"(2^{n - g} amplitudes per GPU, top {g} qubits global; {main['transport']}), "
+                        f"p={args.p} {args.params}; one step = expectation + full adjoint gradient (window chain)",
+            "n": n, "p": args.p, "global_batch": 1, "parallelism": f"statevector sharded x{world}",
+            "value_definition": "steps * 2^(n-30) / max-over-ranks device time: n=30-equivalent E+grad evaluations/s",
+            "l2": f"no flush: {16 * 2 ** (n - g) / 2**30:.0f} GiB per-GPU shard >> 126 MB L2",
+        },
+        "expectation": main["expectation"],
+        "grad_norm_inf": main["grad_norm_inf"],
+        "gpu_launches": int(main["gpu_launches_per_step"] * args.steps),
+        "roofline": main["roofline"],
+        "kernels": main["kernels"],
+        "sharded": {k: v for k, v in main.items() if k not in ("kernels", "roofline", "clocks")},
+        "e2e": {"value": work / (main["wall_ms_per_step"] / 1e3), "unit": UNIT, "h2d_bytes_per_step": 16 * args.p,
+                "d2h_bytes_per_step": 8 * (1 + 2 * args.p),
+                "how": "wall clock around dist.ShardedHandle.value_and_grad (host params in, host E / gradient out), "
+                       "max over ranks"},
+        "clocks": main["clocks"],
+        "other_configs": {"C4_n32_p8": c4} if c4 else {},
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
 
 
 def small_configs() -> dict:
@@ -576,6 +689,12 @@ def run_b200(args, rank: int, world: int, dist) -> None:
 
 def main():
     args = parse()
+    if args.calibrate_cpu:
+        for n in (int(x) for x in args.calibrate_cpu.split(",")):
+            r = oracle_e_plus_grad(n, args.p, args.params)
+            r["scaled_to_30_s"] = scaled(r, N_QUBITS, args.p)
+            print(json.dumps(r), flush=True)
+        return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

@@ -199,6 +199,16 @@ int qsb_shard_visit_run(qsb_ctx* ctx, qsb_table* t, double* v0, double* v1, int 
  * 1 + 2p doubles: <C> (unclamped), d_gamma[p], d_beta[p]. */
 int qsb_small_batch(qsb_ctx* ctx, int count, qsb_table* const* tables, double* const* kets, const int* ps,
                     const double* gammas, const double* betas, int mode, double* out);
+/* Many mid-size registers (12 <= n, each on its own context) -- the paper's
+ * many-graphs regime above the one-CTA size (cli.py bench --jobs runs handles one per
+ * thread).  Instance k: context ctxs[k] (its own CUDA stream), table tables[k], ket /
+ * bra kets[k] / bras[k], depth ps[k], angles concatenated in instance order.  Every
+ * instance's window chain (as qsb_value_and_grad) is issued before any is awaited, so
+ * instances whose sweeps fill only a few SMs (2^(n-12) tiles) run concurrently.
+ * out (host): per instance 1 + 2p doubles: <C> (unclamped), d_gamma[p], d_beta[p]. */
+int qsb_value_and_grad_many(int count, qsb_ctx* const* ctxs, qsb_table* const* tables, double* const* kets,
+                            double* const* bras, const int* ps, const double* gammas, const double* betas,
+                            double* out);
 /* <psi|C|psi> (circuit.expectation_of_state, circuit.py:106-113, without the clamp) */
 int qsb_expectation(qsb_ctx* ctx, qsb_table* t, const double* amps, unsigned flags, double* out);
 /* expectation + adjoint gradient (adjoint.py:37-77): one forward, one backward walk

@@ -94,6 +94,7 @@ _SIGS = {
     "qsb_small_batch": [_vp, _i32, _vp, _vp, _vp, _dp, _dp, _i32, _dp],
     "qsb_sample_descend": [_vp, _vp, _vp, _i32, _u64, _vp, _vp, _vp],
     "qsb_scatter_chunks": [_vp, _vp, _u64, _i32, _vp, _u64],
+    "qsb_value_and_grad_many": [_i32, _vp, _vp, _vp, _vp, _vp, _dp, _dp, _dp],
     "qsb_fill_const": [_vp, _vp, _u64, _dbl, _dbl],
     "qsb_table_detach_values": [_vp],
 }

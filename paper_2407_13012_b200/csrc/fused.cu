@@ -6,6 +6,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <memory>
 
 #include "sweep.cuh"
 
@@ -801,6 +802,69 @@ int qsb_shard_visit_run(qsb_ctx* ctx, qsb_table* t, double* v0, double* v1, int 
 }
 
 }  // extern "C"
+
+namespace {
+// one instance of qsb_value_and_grad_many in flight on its context's stream
+struct Pending {
+  std::unique_ptr<Runner> R;
+  std::vector<Contrib> cs;
+  double* out;
+  int p;
+};
+
+int finish(Pending& q) {
+  std::vector<double> h;
+  QSB_TRY(q.R->fetch(h));
+  collect(*q.R, h, q.cs, q.out, q.out + 1, q.out + 1 + q.p, q.p);
+  q.R.reset();
+  return QSB_OK;
+}
+}  // namespace
+
+extern "C" int qsb_value_and_grad_many(int count, qsb_ctx* const* ctxs, qsb_table* const* tables, double* const* kets,
+                                       double* const* bras, const int* ps, const double* gammas, const double* betas,
+                                       double* out) {
+  if (count < 0 || (count && (!ctxs || !tables || !kets || !bras || !ps || !gammas || !betas || !out)))
+    return invalid("qsb_value_and_grad_many: null argument");
+  std::vector<Pending> pend(count);
+  size_t go = 0, oo = 0;
+  for (int k = 0; k < count; ++k) {
+    qsb_ctx* ctx = ctxs[k];
+    qsb_table* t = tables[k];
+    const int p = ps[k];
+    if (!ctx || !t || !kets[k] || !bras[k]) return invalid("qsb_value_and_grad_many: null instance %d", k);
+    if (p < 1) return invalid("gradient needs depth p >= 1 (instance %d)", k);
+    if (t->n < kSweepT) return invalid("qsb_value_and_grad_many: instance %d has n=%d < 12 (qsb_small_batch)", k, t->n);
+    QSB_CUDA(cudaSetDevice(ctx->device));
+    // a context's partials scratch serves one Runner at a time: complete the previous
+    // instance on the same context before issuing this one
+    for (int j = k - 1; j >= 0; --j)
+      if (ctxs[j] == ctx && pend[j].R) {
+        QSB_TRY(finish(pend[j]));
+        break;
+      }
+    const double* g = gammas + go;
+    const double* b = betas + go;
+    Pending& q = pend[k];
+    q.R.reset(new Runner{ctx, t, t->n, false});
+    q.out = out + oo;
+    q.p = p;
+    QSB_TRY(q.R->init(upper_sweeps(t->n, p)));
+    std::vector<double> scales;
+    std::vector<double2> extras;
+    for (int i = 0; i < p; ++i) scales.push_back(-g[i]);
+    for (int i = 0; i < p; ++i) scales.push_back(g[i]);
+    extras.assign(2 * p, make_double2(1.0, 0.0));
+    QSB_TRY(prepare_luts(t, scales, extras, false));
+    // launches are asynchronous: the next instance is issued while this one runs
+    QSB_TRY(run_chain(*q.R, (double2*)kets[k], (double2*)bras[k], p, g, b, true, true, true, true, q.cs));
+    go += p;
+    oo += 1 + 2 * (size_t)p;
+  }
+  for (int k = 0; k < count; ++k)
+    if (pend[k].R) QSB_TRY(finish(pend[k]));
+  return QSB_OK;
+}
 
 extern "C" {
 

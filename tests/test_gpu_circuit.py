@@ -167,6 +167,29 @@ class TestReferenceBehaviour:
         qs.gradient(h, params)
         assert qs.expectation(h, params) == pytest.approx(before, abs=1e-12)
 
+    @pytest.mark.parametrize("n", [10, 14, 20])
+    def test_state_after_gradient_is_plus(self, n):
+        """adjoint.py:39-42: the gradient leaves the ket at |+>.  The fused walk (n >= 12)
+        does not store its final uncompute -- the buffer is marked |+> and written on the
+        first read, so reads and draws after gradient() / minimize() see |+>."""
+        poly = random_instance(90 + n, n)
+        h = qs.create_handle(poly, backend_name="b200")
+        params = random_params(91, 3)
+        qs.gradient(h, params)
+        plus = np.full(1 << n, 1.0 / np.sqrt(float(1 << n)))
+        assert np.max(np.abs(np.asarray(h.state.data) - plus)) <= 1e-12
+        qs.value_and_grad(h, params)
+        table = oracle.precompute_table(poly.weights, poly.masks, n)
+        want_idx, want_cost = oracle.sample(plus.astype(np.complex128), table, 2000, 4)
+        ss = qs.draw(h, 2000, 4)
+        assert np.array_equal(ss.indices, want_idx) and np.array_equal(ss.costs, want_cost)
+        qs.value_and_grad(h, params)
+        mean = float(np.mean(table))
+        assert circuit.expectation_of_state(h) == pytest.approx(mean, abs=1e-12 * max(1.0, abs(mean)))
+        qs.simulate(h, params)  # a simulate after the pending fill is unaffected
+        psi = oracle.simulate(table, n, params.gammas, params.betas)
+        assert rel_err(np.asarray(h.state.data), psi) <= 1e-10
+
     def test_layer_applications(self, k3_poly):
         h = qs.create_handle(k3_poly, backend_name="b200")
         assert qs.gradient(h, qs.linear_ramp_params(2)).layer_applications == 13
