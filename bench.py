@@ -191,8 +191,8 @@ def _host_ram_ok(n: int) -> bool:
 
 def sample_size(n: int, p: int, target_s: float) -> int:
     """the largest n_s <= n whose measured E+grad should take about target_s (timed once
-    at n=22 -- out of the host caches -- and scaled by 2^(n_s-22) x passes)"""
-    n0 = min(22, n)
+    at n=24 -- out of the host caches -- and scaled by 2^(n_s-24) x passes)"""
+    n0 = min(24, n)
     probe = oracle_e_plus_grad(n0, p)["seconds"]
     n_s = n0
     while n_s < n and probe * 2 ** (n_s + 1 - n0) * _ref_passes(n_s + 1, p) / _ref_passes(n0, p) <= target_s:
@@ -705,8 +705,10 @@ def main():
 
         # QSB_BENCH_DIST_BACKEND / QSB_BENCH_SAME_GPU=1: smoke-test the N>1 paths with
         # several processes on one GPU (gloo host collectives; NCCL needs distinct GPUs)
-        backend = os.environ.get("QSB_BENCH_DIST_BACKEND", "nccl" if torch.cuda.is_available() else "gloo")
-        if os.environ.get("QSB_BENCH_SAME_GPU") == "1":
+        same_gpu = os.environ.get("QSB_BENCH_SAME_GPU") == "1"
+        backend = os.environ.get("QSB_BENCH_DIST_BACKEND",
+                                 "nccl" if torch.cuda.is_available() and not same_gpu else "gloo")
+        if same_gpu:
             local = 0
             os.environ["LOCAL_RANK_DEVICE"] = "0"
         if backend == "nccl":

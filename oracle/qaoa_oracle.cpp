@@ -113,11 +113,13 @@ Pool& pool() {
   return *p;
 }
 
-// static-schedule parallel loop: f(i) for i in [0, n)
+// static-schedule parallel loop: f(i) for i in [0, n); `grain` = iterations below
+// which the loop runs on the calling thread (elementwise loops: 16384 elements; the
+// blocked reductions: a few 2048-element blocks -- numba's prange splits those too)
 template <class F>
-void parallel_for(int64_t n, F f) {
+void parallel_for(int64_t n, F f, int64_t grain = 16384) {
   const int T = threads_now();
-  if (T <= 1 || n < 16384) {
+  if (T <= 1 || n < grain) {
     for (int64_t i = 0; i < n; ++i) f(i);
     return;
   }
@@ -153,15 +155,18 @@ template <class G>
 void tree2(G g, uint64_t len, double* out_re, double* out_im) {
   const uint64_t nb = (len + BLOCK - 1) / BLOCK;
   std::vector<double> pre(nb), pim(nb);
-  parallel_for((int64_t)nb, [&](int64_t b) {
-    double br[BLOCK], bi[BLOCK];
-    memset(br, 0, sizeof(br));
-    memset(bi, 0, sizeof(bi));
-    const uint64_t s = (uint64_t)b * BLOCK, e = std::min(s + BLOCK, len);
-    for (uint64_t i = s; i < e; ++i) g(i, &br[i - s], &bi[i - s]);
-    pre[b] = block_tree(br, BLOCK);
-    pim[b] = block_tree(bi, BLOCK);
-  });
+  parallel_for(
+      (int64_t)nb,
+      [&](int64_t b) {
+        double br[BLOCK], bi[BLOCK];
+        memset(br, 0, sizeof(br));
+        memset(bi, 0, sizeof(bi));
+        const uint64_t s = (uint64_t)b * BLOCK, e = std::min(s + BLOCK, len);
+        for (uint64_t i = s; i < e; ++i) g(i, &br[i - s], &bi[i - s]);
+        pre[b] = block_tree(br, BLOCK);
+        pim[b] = block_tree(bi, BLOCK);
+      },
+      8);
   *out_re = fold(pre);
   *out_im = fold(pim);
 }

@@ -64,7 +64,16 @@ def _run_many(handles, params_list, threads: int):
 
     count = len(handles)
     res: list = [None] * count
-    chunks = [list(range(k, count, threads)) for k in range(min(threads, count))]
+    # instances that share a context (the same handle twice) must be issued by one
+    # thread: its partials scratch serves one walk at a time (the C call serialises them)
+    slot: dict = {}
+    chunks: list = [[] for _ in range(max(1, min(threads, count)))]
+    for i, h in enumerate(handles):
+        key = h.ctx.device.handle.value
+        if key not in slot:
+            slot[key] = len(slot) % len(chunks)
+        chunks[slot[key]].append(i)
+    chunks = [c for c in chunks if c]
     bras = []
     for h in handles:  # the adjoint buffer of each handle (allocated once, kept)
         bras.append(h._adjoint_state())

@@ -2,21 +2,24 @@
 tests/ref/sync_reference_tests.py) against this package -- the drop-in check.
 
 Shim, anchored on the reference's tests/conftest.py:7-11:
-  * `qaoasim` and its submodules resolve to paper_2407_13012_b200 (same names);
-  * the `backend` fixture runs every backend-parametrised test on BACKENDS = ("b200",);
+  * `qaoasim` and its submodules resolve to paper_2407_13012_b200 (same names) through
+    the alias package tests/ref/alias/qaoasim (also on PYTHONPATH for subprocesses);
+  * the `backend` fixture runs every backend-parametrised test on ("b200",), and the
+    CPU kernel-set names the tests hard-code resolve to b200 (see the alias);
   * `qaoasim.kernels.numpy_impl` / `numba_impl` are the oracle and a host-array
     adapter of the b200 kernel set (tests/ref/_kernel_shims.py), so
     test_kernels_parity.py checks B200 against the oracle;
   * every test is marked `gpu` (handles live in HBM);
   * SKIPS lists, with the reason, the tests that assert something only the two CPU
-    kernel sets have (their names, their module objects, numba itself).
-`from conftest import ...` in the copied files resolves to tests/conftest.py, whose
-generators restate the reference conftest's (same streams, same instances)."""
+    kernel sets have (their module objects, the selection between them).
+`from conftest import ...` in the copied files resolves to this module, which
+re-exports tests/conftest.py's generators (restatements of the reference
+conftest's: same streams, same instances)."""
 
 from __future__ import annotations
 
-import importlib
 import importlib.util
+import os
 import sys
 from pathlib import Path
 
@@ -24,38 +27,18 @@ import pytest
 
 ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(Path(__file__).resolve().parent))
 
-import paper_2407_13012_b200 as _pkg  # noqa: E402
+_ALIAS = Path(__file__).resolve().parent / "alias"
+sys.path.insert(0, str(_ALIAS))
+os.environ["PYTHONPATH"] = os.pathsep.join([str(_ALIAS), str(ROOT)] +
+                                          ([os.environ["PYTHONPATH"]] if os.environ.get("PYTHONPATH") else []))
+import qaoasim  # noqa: E402,F401  (tests/ref/alias/qaoasim: the package alias + shims)
 
 BACKENDS = ("b200",)
 
-_SUBMODULES = ("adjoint", "backend", "batch", "circuit", "cli", "costpoly", "errors", "kernels", "optimizer",
-               "problems", "rng", "sampling")
-
-
-def _install_alias() -> None:
-    sys.modules["qaoasim"] = _pkg
-    for name in _SUBMODULES:
-        sys.modules[f"qaoasim.{name}"] = importlib.import_module(f"paper_2407_13012_b200.{name}")
-    from _kernel_shims import make_b200_set, make_oracle_set  # noqa: E402
-
-    oracle_set, b200_set = make_oracle_set(), make_b200_set()
-    import _dense_oracle  # noqa: E402
-
-    sys.modules["qaoasim.oracle"] = _dense_oracle
-    _pkg.oracle = _dense_oracle
-    sys.modules["qaoasim.kernels.numpy_impl"] = oracle_set
-    sys.modules["qaoasim.kernels.numba_impl"] = b200_set
-    _pkg.kernels.numpy_impl = oracle_set
-    _pkg.kernels.numba_impl = b200_set
-
-
-sys.path.insert(0, str(Path(__file__).resolve().parent))
-_install_alias()
-
 # `from conftest import ...` (the copied files, and this repo's own tests once this
-# module holds the name) lands here: re-export every helper of tests/conftest.py, whose
-# generators restate the reference conftest's (same streams, same instances)
+# module holds the name) lands here: re-export every helper of tests/conftest.py
 _spec = importlib.util.spec_from_file_location("_tests_conftest", ROOT / "tests" / "conftest.py")
 _base = importlib.util.module_from_spec(_spec)
 _spec.loader.exec_module(_base)
@@ -66,20 +49,34 @@ for _name in dir(_base):
 # test id (file::name, parametrisation stripped) -> why it cannot apply to a B200 drop-in
 SKIPS = {
     "test_kernels_parity.py::test_samples_identical_across_paths":
-        "draws through create_handle(backend_name='reference'/'accelerated'): CPU kernel-set names",
+        "compares draws of the two CPU kernel sets with each other (here both names are b200)",
     "test_kernels_parity.py::TestSelection::test_env_flag_reference":
-        "QAOA_KERNELS=reference selects the numpy CPU set, which this package replaces",
-    "test_kernels_parity.py::TestSelection::test_env_flag_numpy_alias": "alias of the numpy CPU set",
-    "test_kernels_parity.py::TestSelection::test_env_flag_accelerated": "selects the numba CPU set",
+        "QAOA_KERNELS=reference must select the numpy CPU module, which this package replaces",
+    "test_kernels_parity.py::TestSelection::test_env_flag_numpy_alias": "asserts the numpy CPU module",
+    "test_kernels_parity.py::TestSelection::test_env_flag_accelerated": "asserts the numba CPU module",
     "test_kernels_parity.py::TestSelection::test_auto_prefers_accelerated":
         "auto resolves to b200 here (no CPU sets); asserts the numba module",
-    "test_kernels_parity.py::TestSelection::test_explicit_argument_overrides_env": "CPU set names",
+    "test_kernels_parity.py::TestSelection::test_explicit_argument_overrides_env": "asserts the numpy CPU module",
 }
 
 
 @pytest.fixture(params=BACKENDS)
 def backend(request):
     return request.param
+
+
+@pytest.fixture(autouse=True)
+def _cpu_set_names_resolve_to_b200(request, monkeypatch):
+    """only under the reference's tests: their hard-coded CPU kernel-set names mean
+    "a kernel set" -- resolve them to b200 (and in subprocesses they spawn)"""
+    if Path(__file__).resolve().parent not in Path(str(request.node.fspath)).resolve().parents:
+        return
+    from paper_2407_13012_b200 import cli, kernels
+
+    for name in ("reference", "accelerated", "numpy", "numba"):
+        monkeypatch.setitem(kernels._ALIASES, name, kernels.B200)
+    monkeypatch.setattr(cli, "BACKENDS", ("b200", "gpu", "reference", "accelerated"))
+    monkeypatch.setenv("QSB_REF_ALIAS_NAMES", "1")
 
 
 def pytest_collection_modifyitems(config, items):
