@@ -39,6 +39,9 @@ extern "C" {
 #define QSB_EXACT 1u      /* FMA-free arithmetic + ascending qubit order: bit-identical
                              to the numba kernel set (numba_impl.py:47-72) */
 #define QSB_FROM_PLUS 2u  /* (simulate) start from |+>, the input state is not read */
+#define QSB_HALF_OUT 4u   /* (simulate) a Z2-reduced run may leave the upper half of amps
+                             unwritten (psi(2^(n-1)+y) = psi(2^(n-1)-1-y)); qsb_ctx_last_half
+                             reports it, qsb_state_mirror writes it */
 
 /* fused-op flags of qsb_layer_sweeps (the sweep kernel's SweepFlags) */
 #define QSB_SW_PLUS 1u           /* input is |+> (not read) */
@@ -253,6 +256,14 @@ int qsb_fill_const(qsb_ctx* ctx, double* amps, uint64_t len, double re, double i
  * index (T = vmin + idx, exact for integral tables).  Lets a sharded handle free the
  * 8 B/amp fp64 copy of each layout's table (the caller frees the memory). */
 int qsb_table_detach_values(qsb_table* t);
+/* Z2 reduction (flip-symmetric cost tables, C(x) = C(~x): every MaxCut).  The state
+ * then keeps psi(x) = psi(~x), and the fused paths evolve only x < 2^(n-1).
+ * qsb_table_symmetric: 1 when the table is flip-symmetric bit for bit.
+ * qsb_state_mirror: write the upper half from the lower, psi(2^(n-1)+y) = psi(2^(n-1)-1-y).
+ * qsb_ctx_last_half: 1 when the context's last simulate left the upper half unwritten. */
+int qsb_table_symmetric(qsb_table* t, int* sym);
+int qsb_state_mirror(qsb_ctx* ctx, double* amps, int n);
+int qsb_ctx_last_half(qsb_ctx* ctx, int* half);
 
 #ifdef __cplusplus
 }

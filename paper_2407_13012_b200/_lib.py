@@ -24,6 +24,7 @@ _LIB_PATH = Path(os.environ["QSB_LIB"]) if os.environ.get("QSB_LIB") else Path(_
 QSB_OK, QSB_EINVAL, QSB_ENOMEM, QSB_ECUDA, QSB_ENODEV = 0, 1, 2, 3, 4
 QSB_EXACT = 1
 QSB_FROM_PLUS = 2
+QSB_HALF_OUT = 4
 
 _vp = C.c_void_p
 _u64 = C.c_uint64
@@ -95,6 +96,9 @@ _SIGS = {
     "qsb_sample_descend": [_vp, _vp, _vp, _i32, _u64, _vp, _vp, _vp],
     "qsb_scatter_chunks": [_vp, _vp, _u64, _i32, _vp, _u64],
     "qsb_value_and_grad_many": [_i32, _vp, _vp, _vp, _vp, _vp, _dp, _dp, _dp],
+    "qsb_table_symmetric": [_vp, C.POINTER(_i32)],
+    "qsb_state_mirror": [_vp, _vp, _i32],
+    "qsb_ctx_last_half": [_vp, C.POINTER(_i32)],
     "qsb_fill_const": [_vp, _vp, _u64, _dbl, _dbl],
     "qsb_table_detach_values": [_vp],
 }
@@ -315,6 +319,50 @@ class DeviceArray:
         return NotImplemented
 
     __hash__ = None
+
+    # arithmetic on the host copy (the reference's tests combine table buffers with +,
+    # e.g. test_costpoly.py:78-88); results are host ndarrays
+    def _host(self, other):
+        return other.to_host() if isinstance(other, DeviceArray) else other
+
+    def __add__(self, o):
+        return self.to_host() + self._host(o)
+
+    def __radd__(self, o):
+        return self._host(o) + self.to_host()
+
+    def __sub__(self, o):
+        return self.to_host() - self._host(o)
+
+    def __rsub__(self, o):
+        return self._host(o) - self.to_host()
+
+    def __mul__(self, o):
+        return self.to_host() * self._host(o)
+
+    def __rmul__(self, o):
+        return self._host(o) * self.to_host()
+
+    def __truediv__(self, o):
+        return self.to_host() / self._host(o)
+
+    def __neg__(self):
+        return -self.to_host()
+
+    def __abs__(self):
+        return np.abs(self.to_host())
+
+    def __lt__(self, o):
+        return self.to_host() < self._host(o)
+
+    def __le__(self, o):
+        return self.to_host() <= self._host(o)
+
+    def __gt__(self, o):
+        return self.to_host() > self._host(o)
+
+    def __ge__(self, o):
+        return self.to_host() >= self._host(o)
 
     @property
     def real(self) -> np.ndarray:

@@ -46,6 +46,7 @@ struct qsb_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   uint64_t launches = 0;
   uint64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic issued by the library
+  int last_half = 0;  // the last qsb_simulate_expect (QSB_HALF_OUT) left the upper half unwritten
   // reusable device scratch for reduction partials (grown on demand)
   double* d_scratch = nullptr;
   uint64_t scratch_bytes = 0;
@@ -82,6 +83,7 @@ struct qsb_table {
   double vmin = 0, vmax = 0;
   int kind = 0;               // 0 fp64/sincos, 1 uint8 idx, 2 uint16 idx
   int nvals = 0;              // number of LUT entries (kind 1/2)
+  int sym = 0;                // values[x] == values[len-1-x] for every x (flip-symmetric: Z2 reduction)
   void* cidx = nullptr;       // compact index table (owned)
   double2* d_lut = nullptr;   // phase LUT scratch (owned), up to 65536 entries
   std::vector<double> h_lutbuf;  // host staging

@@ -28,6 +28,7 @@ int small_run(qsb_ctx* ctx, qsb_table* t, double2* ket, int p, const double* gam
 }  // namespace qsb
 
 extern "C" int qsb_table_phase(qsb_ctx* ctx, qsb_table* t, double* amps, double gamma);
+extern "C" int qsb_state_mirror(qsb_ctx* ctx, double* amps, int n);
 extern "C" int qsb_diag_scale(qsb_ctx* ctx, double* amps, const double* table, uint64_t len);
 
 namespace qsb {
@@ -129,9 +130,13 @@ int sweep_family(int nv, int mode, bool is_a) {
 }
 
 // Fill the tile/phase part of SweepArgs for one sweep. Returns the number of gates.
+// n: stored index bits of the arrays; vshift = 1 for a Z2-reduced half statevector,
+// whose B windows sit one stored bit below their (virtual) qubits: qubits 0..10 are
+// stored bits 0..10, qubit 11 is the top qubit n-1 (local bit 11 of the mirror A tile
+// pair), qubits 12.. are stored bits 11.. (sh.lo / sh.hi / sh.glo: qubit numbering)
 int build_shape(const SweepShape& sh, int n, int nv, bool exact, SweepArgs& a, int gates_before_phase[kMaxPhases],
                 const int* pass2 = nullptr, int gates_before_phase2[kMaxPhases] = nullptr, int* gates2 = nullptr,
-                int mode = SM_PLAIN) {
+                int mode = SM_PLAIN, int vshift = 0) {
   int gl[kSweepT];
   for (int i = 0; i < kSweepT; ++i) gl[i] = sh.is_a ? i : (i < 3 ? i : sh.glo + i - 3);
   const int fam = exact ? 4 : sweep_family(nv, mode, sh.is_a);
@@ -141,7 +146,8 @@ int build_shape(const SweepShape& sh, int n, int nv, bool exact, SweepArgs& a, i
   PhaseSpec ps[kMaxPhases];
   for (int p = 0; p < np; ++p) ps[p] = shape_phase(shape, p);
   a.shape = shape;
-  a.glo = sh.is_a ? 3 : sh.glo;
+  const int glo_st = sh.is_a ? 3 : sh.glo - vshift;  // stored bit of B-tile local bit 3
+  a.glo = glo_st;
   const int R = shape_r(shape);
   const int W = shape_w(shape);
   bool applied[kSweepT] = {false};
@@ -191,7 +197,7 @@ int build_shape(const SweepShape& sh, int n, int nv, bool exact, SweepArgs& a, i
     for (int b = 0; b < R; ++b)
       if (gl[5 + W + b] != gl[5 + W] + b) return -1;
   }
-  a.cshift = gl[3];
+  a.cshift = glo_st;
   // tile index -> global base: the non-tile bits as contiguous runs
   a.nruns = 0;
   auto add_run = [&](int pos, int len) {
@@ -204,8 +210,8 @@ int build_shape(const SweepShape& sh, int n, int nv, bool exact, SweepArgs& a, i
   if (sh.is_a) {
     add_run(kSweepT, n - kSweepT);
   } else {
-    add_run(3, sh.glo - 3);
-    add_run(sh.glo + 9, n - sh.glo - 9);
+    add_run(3, glo_st - 3);
+    add_run(glo_st + 9, n - glo_st - 9);
   }
   a.ntiles = 1ull << (n - kSweepT);
   // whole window targeted -> the kernel uses the compile-time masks (shape_apply)
@@ -318,6 +324,13 @@ struct Runner {
   double* partials = nullptr;   // device, kSlots * maxgrid per sweep
   double plus_amp = 0.0;        // 0: 1/sqrt(2^n)
   unsigned maxgrid = 0;
+  // Z2 reduction: the cost table is flip-symmetric (C(x) = C(~x), every MaxCut), so
+  // |+>, the phases and the mixer keep psi(x) = psi(~x); the arrays then hold only
+  // phi(x) = psi(x) for x < 2^(n-1) -- half the HBM bytes and FP64 work of every sweep.
+  // The top qubit's X acts as the complement of all stored bits: the A window visits
+  // tile pairs {T, ~T} (mirror mode), every contraction counts each amplitude twice.
+  bool sym = false;
+  int st() const { return sym ? n - 1 : n; }  // stored index bits
   const qsb_shard_visit* swap = nullptr;  // fused qubit-swap store (sharded walk)
   // Deferred gate scaling (window chain): the factored gates leave a real scale sigma^g
   // on every amplitude; instead of multiplying it out at the end of every sweep, the
@@ -332,8 +345,8 @@ struct Runner {
   int init(int total_sweeps_upper) {
     shapes = plan_sweeps(n);
     unsigned g1, g2;
-    QSB_TRY(sweep_grid(ctx, 1, exact, 1ull << (n - kSweepT), &g1));
-    QSB_TRY(sweep_grid(ctx, 2, exact, 1ull << (n - kSweepT), &g2));
+    QSB_TRY(sweep_grid(ctx, 1, exact, 1ull << (st() - kSweepT), &g1));
+    QSB_TRY(sweep_grid(ctx, 2, exact, 1ull << (st() - kSweepT), &g2));
     maxgrid = std::max(g1, g2);
     QSB_TRY(ensure_scratch(ctx, (uint64_t)total_sweeps_upper * kSlots * maxgrid * sizeof(double) + 64));
     partials = ctx->d_scratch;
@@ -343,7 +356,7 @@ struct Runner {
   // algorithmic HBM bytes of one sweep: every amplitude read/written once, plus
   // one read of the table (compact index or f64) when the sweep has table ops
   double alg_bytes(int nv, int mode, uint32_t flags) const {
-    const double N = (double)(1ull << n);
+    const double N = (double)(1ull << st());
     const double tb = t ? (t->kind == 1 ? 1.0 : t->kind == 2 ? 2.0 : 8.0) : 0.0;
     double b = 0.0;
     if (nv == 1) {
@@ -377,7 +390,8 @@ struct Runner {
     SweepArgs a;
     memset(&a, 0, sizeof(a));
     int gbp[kMaxPhases], gbp2[kMaxPhases] = {0, 0, 0, 0}, gates2 = 0;
-    const int gates = build_shape(sh, n, nv, exact, a, gbp, mode != SM_PLAIN ? pass2 : nullptr, gbp2, &gates2, mode);
+    const int gates = build_shape(sh, st(), nv, exact, a, gbp, mode != SM_PLAIN ? pass2 : nullptr, gbp2, &gates2, mode,
+                                  sym ? 1 : 0);
     if (gates < 0) return invalid("internal: bad sweep layout");
     a.mode = mode;
     {
@@ -391,10 +405,12 @@ struct Runner {
     const bool table_ops = (flags & kTableOps) || mode == SM_BRIDGE;
     a.cmode = (t && t->kind != 0 && table_ops) ? ((!sh.is_a && t->kind == 1) ? 2 : 1) : 0;
     if (!sh.is_a) {  // TMA boxes for the strided B tiles
-      QSB_TRY(encode_b_tile_map(&a.tm0, v0, n, sh.glo));
-      if (nv == 2) QSB_TRY(encode_b_tile_map(&a.tm1, v1, n, sh.glo));
-      if (a.cmode) QSB_TRY(encode_b_cidx_map(&a.tmc, t->cidx, t->kind == 1 ? 1 : 2, n, sh.glo));
+      QSB_TRY(encode_b_tile_map(&a.tm0, v0, st(), a.glo));
+      if (nv == 2) QSB_TRY(encode_b_tile_map(&a.tm1, v1, st(), a.glo));
+      if (a.cmode) QSB_TRY(encode_b_cidx_map(&a.tmc, t->cidx, t->kind == 1 ? 1 : 2, st(), a.glo));
     }
+    a.mirror = (sym && sh.is_a) ? 1 : 0;
+    a.tmask = sym ? (1ull << (st() - 11)) - 1ull : 0ull;
     a.lut = lut;
     a.pre_ang = pre_ang;
     a.pre_extra = pre_extra;
@@ -691,7 +707,8 @@ void collect(const Runner& R, const std::vector<double>& h, const std::vector<Co
   for (int i = 0; i < p && dg; ++i) dg[i] = 0.0;
   for (int i = 0; i < p && db; ++i) db[i] = 0.0;
   for (const Contrib& c : cs) {
-    const double x = Runner::slot_sum(h, R.maxgrid, R.grids, c.sweep, c.slot);
+    // a Z2-reduced sweep sums over half the amplitudes, each standing for two
+    const double x = (R.sym ? 2.0 : 1.0) * Runner::slot_sum(h, R.maxgrid, R.grids, c.sweep, c.slot);
     if (c.kind == 0 && value) *value += x;
     else if (c.kind == 1 && dg) dg[c.layer] += 2.0 * x;
     else if (c.kind == 2 && db) db[c.layer] += -2.0 * x;
@@ -699,6 +716,23 @@ void collect(const Runner& R, const std::vector<double>& h, const std::vector<Co
 }
 
 int upper_sweeps(int n, int p) { return 2 * p * (int)plan_sweeps(n).size() + 4; }
+
+// Z2 reduction applies to fast-mode chains over flip-symmetric tables with n >= 21 (every
+// B window then lies above the A window's 12 qubits); QSB_NO_SYM=1 disables it
+bool env_is(const char* name, const char* dflt) {
+  const char* e = getenv(name);
+  return !e || strcmp(e, dflt) == 0;
+}
+
+bool sym_ok(const qsb_table* t, int n, bool exact) {
+  const char* e = getenv("QSB_NO_SYM");
+  // the mirror A instantiations exist for the default register families (fused.cu
+  // sweep_family) and the staggered bra/ket schedule; A/B experiment overrides of those
+  // run the full vector
+  const bool default_families = env_is("QSB_SWEEP_R1", "6") && env_is("QSB_SWEEP_R2", "4") &&
+                                env_is("QSB_SWEEP_R1M", "4") && env_is("QSB_SWEEP_R2M", "4") && env_is("QSB_STAG", "1");
+  return t && t->sym && !exact && n >= 21 && !(e && atoi(e)) && default_families;
+}
 
 }  // namespace
 
@@ -847,6 +881,7 @@ extern "C" int qsb_value_and_grad_many(int count, qsb_ctx* const* ctxs, qsb_tabl
     const double* b = betas + go;
     Pending& q = pend[k];
     q.R.reset(new Runner{ctx, t, t->n, false});
+    q.R->sym = sym_ok(t, t->n, false);
     q.out = out + oo;
     q.p = p;
     QSB_TRY(q.R->init(upper_sweeps(t->n, p)));
@@ -900,6 +935,8 @@ int qsb_simulate_expect(qsb_ctx* ctx, qsb_table* t, double* amps, int p, const d
     return QSB_OK;
   }
   Runner R{ctx, t, n, exact};
+  R.sym = (flags & QSB_FROM_PLUS) && sym_ok(t, n, exact);
+  ctx->last_half = 0;
   QSB_TRY(R.init(upper_sweeps(n, p)));
   std::vector<double> scales;
   std::vector<double2> extras;
@@ -915,6 +952,10 @@ int qsb_simulate_expect(qsb_ctx* ctx, qsb_table* t, double* amps, int p, const d
       std::vector<double> h;
       QSB_TRY(R.fetch(h));
       collect(R, h, cs, expect_out, nullptr, nullptr, p);
+    }
+    if (R.sym) {  // the upper half: psi(2^(n-1) + y) = phi(2^(n-1) - 1 - y)
+      if (flags & QSB_HALF_OUT) ctx->last_half = 1;
+      else QSB_TRY(qsb_state_mirror(ctx, amps, n));
     }
     return QSB_OK;
   }
@@ -984,6 +1025,7 @@ int qsb_value_and_grad(qsb_ctx* ctx, qsb_table* t, double* ket_, double* bra_, i
     return value_and_grad_perop(ctx, t, ket, bra, p, gammas, betas, flags, skip_forward, value, d_gammas, d_betas);
 
   Runner R{ctx, t, n, false};
+  R.sym = !skip_forward && sym_ok(t, n, false);
   QSB_TRY(R.init(upper_sweeps(n, p)));
   // LUTs: forward phases exp(-i g C) for layers 0..p-1, then inverse phases exp(+i g C) for layers 1..p-1
   std::vector<double> scales;

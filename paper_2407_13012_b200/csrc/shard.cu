@@ -52,6 +52,11 @@ __global__ void __launch_bounds__(kThreads) k_scatter_chunks(const __grid_consta
   }
 }
 
+__global__ void k_state_mirror(double2* amps, uint64_t half) {
+  for (uint64_t y = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; y < half; y += (uint64_t)gridDim.x * blockDim.x)
+    amps[half + y] = qsbd::ld_stream(amps + (half - 1 - y));
+}
+
 __global__ void k_fill_const(double2* amps, uint64_t len, double re, double im) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (uint64_t)gridDim.x * blockDim.x)
     amps[i] = make_double2(re, im);
@@ -92,6 +97,30 @@ int qsb_fill_const(qsb_ctx* ctx, double* amps, uint64_t len, double re, double i
   if (blocks > (uint64_t)ctx->num_sms * 16) blocks = (uint64_t)ctx->num_sms * 16;
   k_fill_const<<<(unsigned)blocks, 256, 0, ctx->stream>>>((double2*)amps, len, re, im);
   QSB_CHECK_LAUNCH(ctx, "fill_const");
+  return QSB_OK;
+}
+
+int qsb_state_mirror(qsb_ctx* ctx, double* amps, int n) {
+  if (!ctx || !amps) return invalid("qsb_state_mirror: null argument");
+  if (n < 1 || n > 62) return invalid("qsb_state_mirror: n=%d out of range", n);
+  QSB_CUDA(cudaSetDevice(ctx->device));
+  const uint64_t half = 1ull << (n - 1);
+  uint64_t blocks = (half + 1023) / 1024;
+  if (blocks > (uint64_t)ctx->num_sms * 16) blocks = (uint64_t)ctx->num_sms * 16;
+  k_state_mirror<<<(unsigned)blocks, 256, 0, ctx->stream>>>((double2*)amps, half);
+  QSB_CHECK_LAUNCH(ctx, "state_mirror");
+  return QSB_OK;
+}
+
+int qsb_ctx_last_half(qsb_ctx* ctx, int* half) {
+  if (!ctx || !half) return invalid("qsb_ctx_last_half: null argument");
+  *half = ctx->last_half;
+  return QSB_OK;
+}
+
+int qsb_table_symmetric(qsb_table* t, int* sym) {
+  if (!t || !sym) return invalid("qsb_table_symmetric: null argument");
+  *sym = t->sym;
   return QSB_OK;
 }
 

@@ -88,6 +88,11 @@ struct SweepArgs {
   int sw_g, sw_rank, sw_nl;
   double2* sw_out[2][8];
   int pair;               // set at launch: this launch is paired (cluster barrier per tile)
+  // Z2-reduced (flip-symmetric) state: the arrays hold the half statevector phi(x) =
+  // psi(x), x < 2^(n-1); an A sweep works on tile pairs {T, T ^ tmask} of 2048
+  // amplitudes with local bit 11 = the top qubit (see kMirBit in sweep_impl.cuh)
+  int mirror;
+  uint64_t tmask;
   double* partials;       // [kSlots][gridDim.x]
   uint64_t ntiles;
   uint32_t flags;

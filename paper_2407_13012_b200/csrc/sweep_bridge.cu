@@ -9,7 +9,7 @@ int launch_sweep_bridge(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
 }
 // second pass staggered (see the kernel)
 int launch_sweep_bridge_t(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
-  if (a.form == GF_FACT_C) return sweepk::launch_merged_f1<2, SM_BRIDGE, GF_FACT_C, SH_A2, SH_B2, 1, true>(ctx, a, g);
-  return sweepk::launch_merged_f1<2, SM_BRIDGE, GF_FACT_S, SH_A2, SH_B2, 1, true>(ctx, a, g);
+  if (a.form == GF_FACT_C) return sweepk::launch_merged_f1<2, SM_BRIDGE, GF_FACT_C, SH_A2, SH_B2, 1, true, true>(ctx, a, g);
+  return sweepk::launch_merged_f1<2, SM_BRIDGE, GF_FACT_S, SH_A2, SH_B2, 1, true, true>(ctx, a, g);
 }
 }  // namespace qsb

@@ -220,7 +220,17 @@ __host__ __device__ constexpr bool stag_local(int sh, int p, int q) {
 // compile-time marker in a kernel's flag mask FM: run a merged bra/ket sweep with the
 // staggered schedule (see the kernel); never set in SweepArgs::flags
 constexpr uint32_t kStagBit = 1u << 30;
-constexpr uint32_t kStagFlags = 0x7fffffffu;  // every flag, staggered (plain sweeps)
+constexpr uint32_t kStagFlags = 0x5fffffffu;  // every flag, staggered (plain sweeps)
+// compile-time marker: an A sweep over a flip-symmetric (Z2-reduced) half statevector.
+// The unit of work is a PAIR of 2048-amplitude tiles {T, ~T} (contiguous 32 KB each):
+// local bits 0..10 are qubits 0..10 within the tile, local bit 11 selects T / ~T and
+// carries the top qubit, whose X acts as the complement of all stored bits -- element
+// (1, l) holds phi(complement(T*2048 + l)), stored at position 2047 - l of tile ~T, so
+// its natural smem position is L ^ 0x7FF.  See SweepArgs::mirror.
+constexpr uint32_t kMirBit = 1u << 29;
+static_assert((kStagFlags & kMirBit) == 0 && (kStagFlags & kStagBit) != 0, "flag-mask markers");
+// the flag mask of a mirror instantiation of FM (0xffffffff = "every flag, no marker")
+constexpr uint32_t mir_mask(uint32_t fm) { return fm == 0xffffffffu ? (0x1fffffffu | kMirBit) : (fm | kMirBit); }
 #ifndef QSB_STAG_EARLY_STORE
 #define QSB_STAG_EARLY_STORE 1  // staggered sweeps store the lead during the lag's last stage
 #endif
@@ -297,6 +307,13 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
   // the next load into a slot waits for the slot's store to be read: A tiles issue it
   // after the first phase, B tiles (slow strided loads) at the tile start
   constexpr bool LATE_ISSUE = TMAST && IS_A;
+  constexpr bool MIR = IS_A && FM != 0xffffffffu && (FM & kMirBit) != 0;
+  static_assert(!MIR || shape_phase(SH, 0).reg_l + R == kSweepT, "mirror: the landing map holds local bit 11 in registers");
+  // natural smem position of local index L (the TMA landing / TMA store layout)
+  auto nat = [](uint32_t L) -> uint32_t {
+    if constexpr (MIR) return (L & 0x800u) ? (L ^ 0x7FFu) : L;
+    else return L;
+  };
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(smem_raw);
   const uint32_t cring_s = ring_s + kRing * kSlotBytes;
@@ -360,7 +377,11 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     }
     mbar_expect_tx(bar, bytes);
     if (vec) {
-      if constexpr (IS_A) {
+      if constexpr (MIR) {  // the pair {T, ~T}: two contiguous 32 KB tiles
+        const double2* src = q == 0 ? a.v0 : a.v1;
+        tma_1d(ring_s + slot * kSlotBytes, src + (tile << 11), kSlotBytes / 2, bar);
+        tma_1d(ring_s + slot * kSlotBytes + kSlotBytes / 2, src + ((tile ^ a.tmask) << 11), kSlotBytes / 2, bar);
+      } else if constexpr (IS_A) {
         const uint64_t base = tile << kSweepT;
         tma_1d(ring_s + slot * kSlotBytes, (q == 0 ? a.v0 : a.v1) + base, kSlotBytes, bar);
       } else {
@@ -372,7 +393,12 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     }
     if (cid) {
       const uint32_t cdst = cring_s + (uint32_t)(k % kRing) * kCBytes;
-      if constexpr (IS_A) {
+      if constexpr (MIR) {  // the pair's table entries, the same natural layout as its amplitudes
+        const uint8_t* cx = (const uint8_t*)a.cidx;
+        const uint32_t esz = cbytes / kTile;
+        tma_1d(cdst, cx + (tile << 11) * esz, cbytes / 2, bar);
+        tma_1d(cdst + cbytes / 2, cx + ((tile ^ a.tmask) << 11) * esz, cbytes / 2, bar);
+      } else if constexpr (IS_A) {
         tma_1d(cdst, (const uint8_t*)a.cidx + (tile << kSweepT) * (cbytes / kTile), cbytes, bar);
       } else {
         const int lowbits = glo - 3;
@@ -412,7 +438,15 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
   const uint64_t iters = a.pair ? (a.ntiles + gridDim.x - 1) / gridDim.x : my_tiles;
   for (uint64_t k = grp; k < iters; k += GR) {
    if (k < my_tiles) {
-    const uint64_t base = tile_base(a, blockIdx.x + k * gridDim.x);
+    const uint64_t tileT = blockIdx.x + k * gridDim.x;
+    const uint64_t base = tile_base(a, tileT);
+    // table views: position of local element l in the smem index tile (the natural
+    // layout) and its stored index (mirror: element (1, l) is stored at 2047 - l of ~T)
+    auto tl = [&](uint32_t l) -> uint32_t { return nat(l); };
+    auto tgi = [&](uint32_t l) -> uint64_t {
+      if constexpr (MIR) return (l & 0x800u) ? ((tileT ^ a.tmask) << 11) + (~l & 0x7FFu) : (tileT << 11) + l;
+      else return base + gofs<IS_A>(l, glo);
+    };
     const uint8_t* cs = cring + (uint32_t)(k % kRing) * kCBytes;
     const uint32_t tb8 = (uint32_t)((blockIdx.x + k * gridDim.x) & 1u) << 3;  // cmode 2: tile's half of each row
     constexpr PhaseSpec P0 = shape_phase(SH, 0);
@@ -426,27 +460,26 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
       if constexpr (GR == 1 && !LATE_ISSUE) issue(k + 2);  // (LATE_ISSUE: after the first phase)
       wait_seq(k);
       xs_addr = ring_s + (uint32_t)(k % kRing) * kSlotBytes;
-      const uint32_t p0 = xs_addr + lb * 16u;  // natural (TMA) layout
       const bool plus = flags & SF_PLUS;
 #pragma unroll
-      for (int j = 0; j < NR; ++j) {
-        const double2 x = lds(p0 + (((uint32_t)j << P0.reg_l) * 16u));
+      for (int j = 0; j < NR; ++j) {  // natural (TMA) layout
+        const double2 x = lds(xs_addr + nat(lb | ((uint32_t)j << P0.reg_l)) * 16u);
         v[0][j] = make_double2(plus ? a.plus_amp : x.x, plus ? 0.0 : x.y);
       }
+      if constexpr (MIR) gsync();  // the mirror half was read from other warps' chunks
     } else {
       xb_addr = ring_s + (uint32_t)((2 * k) % kRing) * kSlotBytes;
       xs_addr = ring_s + (uint32_t)((2 * k + 1) % kRing) * kSlotBytes;
       wait_seq(2 * k);
       if constexpr (MODE != SM_BRIDGE) {
-        const uint32_t pb = xb_addr + lb * 16u;
 #pragma unroll
-        for (int j = 0; j < NR; ++j) v[1][j] = lds(pb + (((uint32_t)j << P0.reg_l) * 16u));
+        for (int j = 0; j < NR; ++j) v[1][j] = lds(xb_addr + nat(lb | ((uint32_t)j << P0.reg_l)) * 16u);
       }
       if constexpr (!STAG1) {  // staggered: the ket lands in stage 0
         wait_seq(2 * k + 1);
-        const uint32_t p0 = xs_addr + lb * 16u;
 #pragma unroll
-        for (int j = 0; j < NR; ++j) v[0][j] = lds(p0 + (((uint32_t)j << P0.reg_l) * 16u));
+        for (int j = 0; j < NR; ++j) v[0][j] = lds(xs_addr + nat(lb | ((uint32_t)j << P0.reg_l)) * 16u);
+        if constexpr (MIR) gsync();
       }
     }
 
@@ -502,19 +535,20 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     // ---------------------------------------------------------------- pre ops
     if constexpr (MODE == SM_PLAIN) {
       auto pre_ops = [&](auto tv) {
-        const uint64_t g0 = base + gofs<IS_A>(lb, glo);
         if constexpr (NV == 2) {
           if (flags & SF_BRA_FROM_KET) {
 #pragma unroll
             for (int j = 0; j < NR; ++j) {
-              const double t = tv.val(lb | ((uint32_t)j << P0.reg_l), g0 + gofs<IS_A>((uint32_t)j << P0.reg_l, glo));
+              const uint32_t l = lb | ((uint32_t)j << P0.reg_l);
+              const double t = tv.val(tl(l), tgi(l));
               v[1][j] = make_double2(t * v[0][j].x, t * v[0][j].y);
             }
           }
           if (flags & SF_PRE_DINNER) {
 #pragma unroll
             for (int j = 0; j < NR; ++j) {
-              const double t = tv.val(lb | ((uint32_t)j << P0.reg_l), g0 + gofs<IS_A>((uint32_t)j << P0.reg_l, glo));
+              const uint32_t l = lb | ((uint32_t)j << P0.reg_l);
+              const double t = tv.val(tl(l), tgi(l));
               const double d = v[1][j].x * v[0][j].y - v[1][j].y * v[0][j].x;
               if (j & 1) acc1b = fma(t, d, acc1b);
               else acc1 = fma(t, d, acc1);
@@ -524,7 +558,8 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
         if (flags & SF_PRE_PHASE) {
 #pragma unroll
           for (int j = 0; j < NR; ++j) {
-            const double2 f = tv.phase(lb | ((uint32_t)j << P0.reg_l), g0 + gofs<IS_A>((uint32_t)j << P0.reg_l, glo));
+            const uint32_t l = lb | ((uint32_t)j << P0.reg_l);
+            const double2 f = tv.phase(tl(l), tgi(l));
 #pragma unroll
             for (int q = 0; q < NV; ++q) v[q][j] = cmul<EXACT>(v[q][j], f);
           }
@@ -606,11 +641,11 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     auto mid_ops = [&](uint32_t lbm) {
       constexpr int RM = shape_phase(SH, NP - 1).reg_l;
       with_table([&](auto tv) {
-        const uint64_t g1 = base + gofs<IS_A>(lbm, glo);
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
-          const uint32_t l = lbm | ((uint32_t)j << RM);
-          const uint64_t g = g1 + gofs<IS_A>((uint32_t)j << RM, glo);
+          const uint32_t lf = lbm | ((uint32_t)j << RM);
+          const uint32_t l = tl(lf);
+          const uint64_t g = tgi(lf);
           if constexpr (MODE == SM_BRIDGE) {
             const double t = tv.val(l, g);
             if (flags & SF_MID_EXPECT) {
@@ -660,8 +695,17 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
       for (int j = 0; j < NR; ++j) v[q][j] = make_double2(v[q][j].x * sc, v[q][j].y * sc);
     };
     auto store_vec = [&](int q) {
-      uint64_t g1 = base + gofs<IS_A>(lb, glo);
       double2* dst = q == 0 ? a.v0 : a.v1;
+      if constexpr (MIR) {  // element (m, l): tile T at l, or tile ~T at 2047 - l
+        const uint64_t t0 = tileT << 11, t1 = (tileT ^ a.tmask) << 11;
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+          const uint32_t L = lb | ((uint32_t)j << RL);
+          st_stream(dst + ((L & 0x800u) ? t1 + (~L & 0x7FFu) : t0 + L), v[q][j]);
+        }
+        return;
+      }
+      uint64_t g1 = base + gofs<IS_A>(lb, glo);
       if (a.sw_g) {  // qubit swap fused into the store: the whole tile goes to shard c
         const int hb = a.sw_nl - a.sw_g;
         const uint64_t c = base >> hb;
@@ -744,9 +788,9 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
         gates(QLc{});
         if constexpr (s == 0 && MODE == SM_MERGED) {  // the lag lands (natural layout)
           wait_seq(2 * k + 1);
-          const uint32_t p0 = xs_addr + lb * 16u;
 #pragma unroll
-          for (int j = 0; j < NR; ++j) v[0][j] = lds(p0 + (((uint32_t)j << M.reg_l) * 16u));
+          for (int j = 0; j < NR; ++j) v[0][j] = lds(xs_addr + nat(lb | ((uint32_t)j << M.reg_l)) * 16u);
+          if constexpr (MIR) gsync();  // before the first exchange stores into either slot
         } else if constexpr (s != SREG) {
           constexpr int pp = s - 1 < NP ? s - 1 : 2 * NP - s;  // map of stage s-1
           xload(QGc{}, M, std::integral_constant<bool, stag_local<W>(SH, pp, p)>{});
@@ -790,10 +834,10 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     if constexpr (MODE == SM_PLAIN) {
       // post ops: <psi|C|psi> (NV=1) or <bra|C|ket> (NV=2) after the gates, in the last map
       if (flags & (SF_POST_EXPECT | SF_POST_DINNER)) with_table([&](auto tv) {
-        const uint64_t g1 = base + gofs<IS_A>(lb, glo);
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
-          const double t = tv.val(lb | ((uint32_t)j << RL), g1 + gofs<IS_A>((uint32_t)j << RL, glo));
+          const uint32_t l = lb | ((uint32_t)j << RL);
+          const double t = tv.val(tl(l), tgi(l));
           double d;
           if constexpr (NV == 1) d = fma(v[0][j].x, v[0][j].x, v[0][j].y * v[0][j].y);
           else d = v[1][j].x * v[0][j].y - v[1][j].y * v[0][j].x;  // slot 0: PRE_DINNER may use slot 1
@@ -810,9 +854,10 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
       // natural layout (the final map puts quarter-warp lanes on local bits 0..2:
       // conflict-free, and each 8-amplitude chunk is the warp's own -- a warp barrier
       // orders it after the last exchange's reads)
-      __syncwarp();
+      if constexpr (MIR) gsync();  // the mirror half lands in other warps' chunks
+      else __syncwarp();
 #pragma unroll
-      for (int j = 0; j < NR; ++j) sts(xs_addr + (lb | ((uint32_t)j << RL)) * 16u, v[0][j]);
+      for (int j = 0; j < NR; ++j) sts(xs_addr + nat(lb | ((uint32_t)j << RL)) * 16u, v[0][j]);
     }
     if constexpr (NV == 1) fence_proxy_async();
     if (!(flags & SF_NO_STORE) && !tma_out) {
@@ -827,7 +872,10 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
       if constexpr (TMAST) {
         if (tma_out && tid == 0) {
           const uint64_t tile = blockIdx.x + k * gridDim.x;
-          if constexpr (IS_A) {
+          if constexpr (MIR) {
+            tma_store_1d(a.v0 + (tile << 11), xs_addr, kSlotBytes / 2);
+            tma_store_1d(a.v0 + ((tile ^ a.tmask) << 11), xs_addr + kSlotBytes / 2, kSlotBytes / 2);
+          } else if constexpr (IS_A) {
             tma_store_1d(a.v0 + (tile << kSweepT), xs_addr, kSlotBytes);
           } else {
             const int lowbits = glo - 3;
@@ -946,7 +994,7 @@ struct SweepKernel {
 
 // fast-mode instantiations of one register family (A shape SA, B shape SB, GR warp
 // groups; FMX = kStagFlags: the staggered bra/ket schedule).  A sweeps always cover their whole 12-bit window; B windows may be partial.
-template <int NV, int SA, int SB, int GR = 1, uint32_t FMX = 0xffffffffu>
+template <int NV, int SA, int SB, int GR = 1, uint32_t FMX = 0xffffffffu, bool WM = false>
 int launch_fast(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
   auto L = [&](auto k) { return decltype(k)::launch(ctx, a, g); };
   const bool ksin = a.kind == 0;
@@ -955,6 +1003,21 @@ int launch_fast(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
   // lean instantiation: whole window, gates only -- the chain's mid-layer forward
   // sweeps (for bra/ket sweeps the lean variant measured slower: not used)
   constexpr uint32_t LEAN = SF_POST_SCALE;
+  if (a.mirror && a.shape == SA) {  // Z2-reduced half statevector (whole A window only)
+    if constexpr (WM) {
+      if (!a.full) return invalid("internal: mirror A sweeps gate the whole window");
+      constexpr uint32_t FM = mir_mask(FMX);
+      if constexpr (NV == 1) {
+        if ((a.flags & ~LEAN) == 0)
+          return c ? L(SweepKernel<SA, NV, C, false, true, P, C, GR, LEAN | kMirBit>{})
+                   : L(SweepKernel<SA, NV, S, false, true, P, S, GR, LEAN | kMirBit>{});
+      }
+      if (c) return ksin ? L(SweepKernel<SA, NV, C, true, true, P, C, GR, FM>{}) : L(SweepKernel<SA, NV, C, false, true, P, C, GR, FM>{});
+      return ksin ? L(SweepKernel<SA, NV, S, true, true, P, S, GR, FM>{}) : L(SweepKernel<SA, NV, S, false, true, P, S, GR, FM>{});
+    } else {
+      return invalid("internal: this sweep family has no mirror (Z2-reduced) A instantiation");
+    }
+  }
   if constexpr (NV == 1) {
     if (a.full && (a.flags & ~LEAN) == 0) {
       if (a.shape == SA) return c ? L(SweepKernel<SA, NV, C, false, true, P, C, GR, LEAN>{})
@@ -977,7 +1040,7 @@ int launch_fast(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
 
 // merged / bridge instantiations (fast mode; shapes SA / SB of one register family).  Table ops between
 // the passes dispatch on the table kind at run time (KSIN = false).
-template <int NV, int MODE, int F1, int SA = SH_A2, int SB = SH_B2, int GR = 1, bool STG = false>
+template <int NV, int MODE, int F1, int SA = SH_A2, int SB = SH_B2, int GR = 1, bool STG = false, bool WM = false>
 int launch_merged_f1(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
   auto L = [&](auto k) { return decltype(k)::launch(ctx, a, g); };
   // every flag a merged / bridge sweep of this kind can carry (run_chain, fused.cu)
@@ -988,6 +1051,17 @@ int launch_merged_f1(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
   constexpr uint32_t M = M0 | (STG ? kStagBit : 0u);
   if ((a.flags & ~M0) != 0) return invalid("internal: unexpected flags 0x%x for a merged sweep", a.flags);
   const bool c2 = a.form2 == GF_FACT_C;
+  if (a.mirror && a.shape == SA) {  // Z2-reduced half statevector (whole A window only)
+    if constexpr (WM) {
+      constexpr uint32_t MM = M | kMirBit;
+      if (!a.full) return invalid("internal: mirror A sweeps gate the whole window");
+      if constexpr (MODE == SM_BRIDGE) return L(SweepKernel<SA, NV, F1, false, true, MODE, F1, GR, MM>{});
+      else return c2 ? L(SweepKernel<SA, NV, F1, false, true, MODE, GF_FACT_C, GR, MM>{})
+                     : L(SweepKernel<SA, NV, F1, false, true, MODE, GF_FACT_S, GR, MM>{});
+    } else {
+      return invalid("internal: this sweep family has no mirror (Z2-reduced) A instantiation");
+    }
+  }
   if constexpr (MODE == SM_BRIDGE) {  // Rx(-2b) then Rx(+2b): the same form
     if (a.shape == SA) return a.full ? L(SweepKernel<SA, NV, F1, false, true, MODE, F1, GR, M>{})
                                         : L(SweepKernel<SA, NV, F1, false, false, MODE, F1, GR, M>{});

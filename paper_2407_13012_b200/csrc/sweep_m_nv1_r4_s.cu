@@ -3,6 +3,6 @@
 
 namespace qsb {
 int launch_sweep_m_nv1_r4_s(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
-  return sweepk::launch_merged_f1<1, SM_MERGED, GF_FACT_S, SH_A2, SH_B2>(ctx, a, g);
+  return sweepk::launch_merged_f1<1, SM_MERGED, GF_FACT_S, SH_A2, SH_B2, 1, false, true>(ctx, a, g);
 }
 }  // namespace qsb

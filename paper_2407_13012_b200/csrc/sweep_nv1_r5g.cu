@@ -4,6 +4,6 @@
 
 namespace qsb {
 int launch_sweep_nv1_r5g(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
-  return sweepk::launch_fast<1, SH_A1, SH_B1, 2>(ctx, a, g);
+  return sweepk::launch_fast<1, SH_A1, SH_B1, 2, 0xffffffffu, true>(ctx, a, g);
 }
 }  // namespace qsb

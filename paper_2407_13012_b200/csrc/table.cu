@@ -113,8 +113,29 @@ static int precompute_into(qsb_ctx* ctx, const double* weights, const int64_t* m
   return QSB_OK;
 }
 
+// flip symmetry check: bad = 1 unless v[x] == v[len-1-x] for every x
+__global__ void k_symcheck(const double* __restrict__ v, uint64_t len, int* bad) {
+  const uint64_t half = len >> 1;
+  bool ok = true;
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < half; x += (uint64_t)gridDim.x * blockDim.x)
+    ok = ok && (v[x] == v[len - 1 - x]);
+  if (!__syncthreads_and(ok) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
 static int finish_table(qsb_ctx* ctx, qsb_table* t) {
   QSB_TRY(minmax(ctx, t->values, t->len, &t->vmin, &t->vmax));
+  t->sym = 0;
+  if (t->len >= 2) {
+    QSB_TRY(ensure_scratch(ctx, 64));
+    int* bad = (int*)ctx->d_scratch;
+    QSB_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+    k_symcheck<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(t->values, t->len, bad);
+    QSB_CHECK_LAUNCH(ctx, "symmetry check");
+    int hbad = 1;
+    QSB_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    t->sym = hbad ? 0 : 1;
+  }
   t->kind = 0;
   t->nvals = 0;
   const double range = t->vmax - t->vmin;

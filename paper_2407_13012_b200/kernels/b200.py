@@ -180,17 +180,40 @@ def _params(gammas, betas):
     return g, b
 
 
-def simulate(amps: DeviceArray, table: DeviceArray, n: int, gammas, betas, *, exact: bool, want_expectation: bool):
-    """Reset to |+>, then p phase/mixer layers; optionally return <C> from the last sweep."""
+def simulate(amps: DeviceArray, table: DeviceArray, n: int, gammas, betas, *, exact: bool, want_expectation: bool,
+             half_ok: bool = False):
+    """Reset to |+>, then p phase/mixer layers; optionally return <C> from the last sweep.
+
+    half_ok: a Z2-reduced run (flip-symmetric table) may leave the upper half of amps
+    unwritten -- returns (value, half) then, half = True when it did (mirror_state
+    writes it)."""
     th = ensure_table_handle(table, n)
     g, b = _params(gammas, betas)
-    flags = _lib.QSB_FROM_PLUS | (_lib.QSB_EXACT if exact else 0)
+    flags = _lib.QSB_FROM_PLUS | (_lib.QSB_EXACT if exact else 0) | (_lib.QSB_HALF_OUT if half_ok else 0)
     e = C.c_double()
     call(
         "qsb_simulate_expect", _h(amps), th.ptr, amps.ptr, g.shape[0], _lib.f64_ptr(g), _lib.f64_ptr(b), flags,
         C.byref(e) if want_expectation else None,
     )
-    return e.value if want_expectation else None
+    value = e.value if want_expectation else None
+    if not half_ok:
+        return value
+    half = C.c_int()
+    call("qsb_ctx_last_half", _h(amps), C.byref(half))
+    return value, bool(half.value)
+
+
+def mirror_state(amps: DeviceArray, n: int) -> None:
+    """psi(2^(n-1) + y) = psi(2^(n-1) - 1 - y): the upper half of a Z2-reduced state."""
+    call("qsb_state_mirror", _h(amps), amps.ptr, int(n))
+
+
+def table_symmetric(table: DeviceArray, n: int) -> bool:
+    """the cost table is flip-symmetric bit for bit (C(x) = C(~x))"""
+    th = ensure_table_handle(table, n)
+    out = C.c_int()
+    call("qsb_table_symmetric", th.ptr, C.byref(out))
+    return bool(out.value)
 
 
 def expectation(amps: DeviceArray, table: DeviceArray, n: int) -> float:

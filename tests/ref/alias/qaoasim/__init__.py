@@ -36,12 +36,16 @@ def map_cpu_set_names() -> None:
     for name in CPU_SET_NAMES:
         _kernels._ALIASES[name] = _kernels.B200
     _cli.BACKENDS = ("b200", "gpu", "reference", "accelerated")
+    if "qaoasim.cli" in sys.modules:
+        sys.modules["qaoasim.cli"].BACKENDS = _cli.BACKENDS
 
 
 if __import__("os").environ.get("QSB_REF_ALIAS_NAMES") == "1":
     map_cpu_set_names()
 
-for _name in ("adjoint", "backend", "batch", "circuit", "cli", "costpoly", "errors", "kernels", "optimizer",
+# (cli is not pre-registered: `python -m qaoasim.cli` must load it through this
+# package's path -- a second copy of paper_2407_13012_b200/cli.py named qaoasim.cli)
+for _name in ("adjoint", "backend", "batch", "circuit", "costpoly", "errors", "kernels", "optimizer",
               "problems", "rng", "sampling"):
     sys.modules[f"qaoasim.{_name}"] = importlib.import_module(f"paper_2407_13012_b200.{_name}")
 

@@ -1,0 +1,69 @@
+"""Z2 reduction (flip-symmetric cost tables: every MaxCut): the fused chains evolve
+only x < 2^(n-1) (psi(x) = psi(~x)), the A window on tile pairs {T, ~T}.  Checked
+against the CPU oracle and against the full (QSB_NO_SYM=1) fast path."""
+
+import numpy as np
+import pytest
+
+import paper_2407_13012_b200 as qs
+from paper_2407_13012_b200.kernels import b200
+
+from conftest import random_instance, random_params, rel_err
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def test_symmetry_detection():
+    h = qs.create_handle(qs.maxcut_polynomial(qs.random_regular(22, 3, seed=1)), backend_name="b200")
+    assert b200.table_symmetric(h.table.values.data, 22)
+    qubo = qs.Polynomial(22, [(0.5, 1 << 3), (1.25, (1 << 4) | (1 << 9))])
+    h2 = qs.create_handle(qubo, backend_name="b200")
+    assert not b200.table_symmetric(h2.table.values.data, 22)
+    h.close()
+    h2.close()
+
+
+@pytest.mark.parametrize("n,p,seed", [(21, 3, 1), (22, 1, 2), (23, 4, 3), (24, 2, 4), (26, 3, 5)])
+def test_reduced_chain_vs_oracle_and_full(n, p, seed, monkeypatch):
+    poly = random_instance(900 + seed, n)
+    params = random_params(seed, p)
+    table = oracle.precompute_table(poly.weights, poly.masks, n)
+    e, dg, db = oracle.value_and_grad(table, n, params.gammas, params.betas)
+    psi = oracle.simulate(table, n, params.gammas, params.betas)
+    h = qs.create_handle(poly, backend_name="b200")
+    assert b200.table_symmetric(h.table.values.data, n)
+    v, g = qs.value_and_grad(h, params)
+    assert abs(v - e) <= 1e-10 * max(1.0, abs(e))
+    got = np.concatenate([g.d_gammas, g.d_betas])
+    assert rel_err(got, np.concatenate([dg, db])) <= 1e-10
+    ev = qs.expectation(h, params)
+    assert abs(ev - e) <= 1e-10 * max(1.0, abs(e))
+    st = qs.statevector(h, params)  # the mirror half is written on this read
+    assert rel_err(st, psi) <= 1e-10
+    assert np.array_equal(st[: 1 << (n - 1)], st[::-1][: 1 << (n - 1)])  # psi(x) == psi(~x) bit for bit
+    qs.simulate(h, params)
+    ss = qs.draw(h, 3000, 9)
+    idx, cost = oracle.sample(np.asarray(h.state.data), table, 3000, 9)
+    assert np.array_equal(ss.indices, idx) and np.array_equal(ss.costs, cost)
+    monkeypatch.setenv("QSB_NO_SYM", "1")
+    v1, g1 = qs.value_and_grad(h, params)
+    assert abs(v1 - v) <= 1e-12 * max(1.0, abs(v))
+    assert rel_err(np.concatenate([g1.d_gammas, g1.d_betas]), got) <= 1e-12
+    h.close()
+
+
+def test_reduced_batch_many():
+    from paper_2407_13012_b200 import batch
+
+    polys = [random_instance(950 + k, 21 + k % 2) for k in range(4)]
+    params = [random_params(60 + k, 2) for k in range(4)]
+    hs = [qs.create_handle(pl, backend_name="b200") for pl in polys]
+    got = batch.value_and_grad_batch(hs, params)
+    for pl, prm, (v, g) in zip(polys, params, got):
+        table = oracle.precompute_table(pl.weights, pl.masks, pl.n)
+        e, dg, db = oracle.value_and_grad(table, pl.n, prm.gammas, prm.betas)
+        assert abs(v - min(max(e, table.min()), table.max())) <= 1e-10 * max(1.0, abs(e))
+        assert rel_err(np.concatenate([g.d_gammas, g.d_betas]), np.concatenate([dg, db])) <= 1e-10
+    for h in hs:
+        h.close()
