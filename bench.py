@@ -586,8 +586,10 @@ def run_b200(args, rank: int, world: int, dist) -> None:
     layers_per_s = args.p * args.steps / (sim_ms / 1e3)
 
     # C3's 10^6 shots: draw from the simulated state (probability tree + per-shot
-    # descent + cost gather on the device; indices/costs copied to the host)
+    # descent + cost gather on the device; indices/costs copied to the host).  One
+    # untimed warm-up draw allocates the context's sampler scratch (~0.1 s once).
     qs.simulate(h, params)
+    qs.draw(h, 1000, 0)
     dev.sync()
     dev.timer_start()
     t0 = time.perf_counter()

@@ -111,7 +111,11 @@ int qsb_ctx_xfer(qsb_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
 int qsb_ctx_launches(qsb_ctx* ctx, uint64_t* out);
 
 /* ----------------------------------------------------- memory (backend.py allocation hooks) */
+/* buffers <= 1 GiB come from the device's stream-ordered pool (cudaMallocAsync on the
+ * context stream; QSB_NO_MEMPOOL=1: cudaMalloc); qsb_alloc_ipc always uses cudaMalloc
+ * (buffers exported with qsb_ipc_handle) */
 int qsb_alloc(qsb_ctx* ctx, uint64_t bytes, void** dptr);            /* np.empty, backend.py:133,165 */
+int qsb_alloc_ipc(qsb_ctx* ctx, uint64_t bytes, void** dptr);
 int qsb_free(qsb_ctx* ctx, void* dptr);                              /* eager release (StateBuffer.free) */
 /* CUDA IPC of device buffers for the sharded walk's fused qubit swap (dist.py):
  * export a 64-byte handle, open a peer process's buffer, close it; qsb_device_sync

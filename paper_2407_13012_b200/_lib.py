@@ -49,6 +49,7 @@ _SIGS = {
     "qsb_prof_begin": [_vp],
     "qsb_prof_end": [_vp, _dp, _i32],
     "qsb_alloc": [_vp, _u64, C.POINTER(_vp)],
+    "qsb_alloc_ipc": [_vp, _u64, C.POINTER(_vp)],
     "qsb_free": [_vp, _vp],
     "qsb_h2d": [_vp, _vp, _vp, _u64],
     "qsb_d2h": [_vp, _vp, _vp, _u64],
@@ -246,13 +247,16 @@ class DeviceArray:
 
     __slots__ = ("dctx", "ptr", "dtype", "length", "table", "__weakref__")
 
-    def __init__(self, dctx: DeviceContext, length: int, dtype):
+    def __init__(self, dctx: DeviceContext, length: int, dtype, ipc: bool = False):
+        """ipc=True: plain cudaMalloc memory that can be exported to peer processes
+        (qsb_ipc_handle); otherwise buffers <= 1 GiB come from the stream-ordered pool."""
         self.dctx = dctx
         self.dtype = np.dtype(dtype)
         self.length = int(length)
         self.table = None  # attached qsb_table handle for cost tables
         p = _vp()
-        check(load().qsb_alloc(dctx.handle, self.nbytes, C.byref(p)), "device allocation")
+        fn = load().qsb_alloc_ipc if ipc else load().qsb_alloc
+        check(fn(dctx.handle, self.nbytes, C.byref(p)), "device allocation")
         self.ptr = p.value
 
     # -- ndarray-like surface

@@ -42,6 +42,8 @@ def _run(handles, params_list, mode: int):
         tables.append(b200.ensure_table_handle(h.table.values.data, h.n).ptr)
         kets.append(h.state.data.ptr)
         ps.append(prm.p)
+    for h in handles:  # their buffers were last touched on their own streams
+        h.ctx.synchronize()
     gam = np.ascontiguousarray(np.concatenate([np.asarray(p.gammas, dtype=np.float64) for p in params_list]))
     bet = np.ascontiguousarray(np.concatenate([np.asarray(p.betas, dtype=np.float64) for p in params_list]))
     out = np.empty(sum(1 + 2 * p for p in ps), dtype=np.float64)

@@ -3,6 +3,10 @@
 #include <math.h>
 #include <string.h>
 
+#include <stdlib.h>
+
+#include <unordered_set>
+
 #include "common.cuh"
 
 namespace {
@@ -126,21 +130,60 @@ int qsb_device_count(int* out) {
   return QSB_OK;
 }
 
+// Context pool: creating a context costs 5-30 ms (stream, events, pinned staging,
+// device queries) -- more than a whole small-register E+grad.  Destroyed contexts go
+// back to a per-device free list with their stream, events, pinned buffer and small
+// scratch (the sampler's large scratch is released) and qsb_ctx_create reuses them.
+namespace {
+constexpr size_t kPoolCap = 32;
+std::mutex g_pool_mu;
+std::vector<qsb_ctx*> g_pool[qsb::kMaxDevices];
+
+struct DevInfo {
+  cudaError_t err;
+  int major, sms;
+};
+qsb::PerDevice<DevInfo> g_devinfo;
+
+void reset_for_reuse(qsb_ctx* ctx) {
+  ctx->launches = 0;
+  ctx->h2d_bytes = ctx->d2h_bytes = 0;
+  ctx->last_half = 0;
+  ctx->tree_n = -1;
+  ctx->tree_amps = nullptr;
+  ctx->prof = false;
+  ctx->prof_recs.clear();
+  ctx->prof_used = 0;
+}
+}  // namespace
+
 int qsb_ctx_create(int device, qsb_ctx** out) {
   if (!out) return invalid("qsb_ctx_create: null out");
   *out = nullptr;
+  if (device < 0 || device >= kMaxDevices) return invalid("qsb_ctx_create: device %d out of range", device);
   QSB_CUDA(cudaSetDevice(device));
+  {
+    std::lock_guard<std::mutex> g(g_pool_mu);
+    if (!g_pool[device].empty()) {
+      qsb_ctx* ctx = g_pool[device].back();
+      g_pool[device].pop_back();
+      reset_for_reuse(ctx);
+      *out = ctx;
+      return QSB_OK;
+    }
+  }
+  const DevInfo& info = g_devinfo.get(device, [&] {
+    DevInfo d{cudaSuccess, 0, 0};
+    d.err = cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, device);
+    if (d.err == cudaSuccess) d.err = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, device);
+    return d;
+  });
+  QSB_CUDA(info.err);
+  if (info.major < 10) return invalid("device %d is sm_%dx; libqsb is built for sm_100a (B200)", device, info.major);
   qsb_ctx* ctx = new qsb_ctx();
   ctx->device = device;
-  cudaDeviceProp prop;
-  cudaError_t e = cudaGetDeviceProperties(&prop, device);
-  if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "cudaGetDeviceProperties"); }
-  if (prop.major < 10) {
-    delete ctx;
-    return invalid("device %d is sm_%d%d; libqsb is built for sm_100a (B200)", device, prop.major, prop.minor);
-  }
-  ctx->num_sms = prop.multiProcessorCount;
-  e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  ctx->num_sms = info.sms;
+  cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev1);
   if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_small, 4096 * sizeof(double));
@@ -149,8 +192,7 @@ int qsb_ctx_create(int device, qsb_ctx** out) {
   return QSB_OK;
 }
 
-int qsb_ctx_destroy(qsb_ctx* ctx) {
-  if (!ctx) return QSB_OK;
+static void destroy_now(qsb_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->d_scratch) cudaFree(ctx->d_scratch);
@@ -163,6 +205,30 @@ int qsb_ctx_destroy(qsb_ctx* ctx) {
   for (cudaEvent_t e : ctx->prof_pool) cudaEventDestroy(e);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
+}
+
+int qsb_ctx_destroy(qsb_ctx* ctx) {
+  if (!ctx) return QSB_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  // the sampler's scratch is sized by the largest state drawn (0.5 GB at n=30): release it
+  if (ctx->d_sample) cudaFree(ctx->d_sample);
+  if (ctx->d_shots) cudaFree(ctx->d_shots);
+  ctx->d_sample = ctx->d_shots = nullptr;
+  ctx->sample_bytes = ctx->shots_bytes = 0;
+  if (ctx->scratch_bytes > (64u << 20)) {
+    cudaFree(ctx->d_scratch);
+    ctx->d_scratch = nullptr;
+    ctx->scratch_bytes = 0;
+  }
+  {
+    std::lock_guard<std::mutex> g(g_pool_mu);
+    if (g_pool[ctx->device].size() < kPoolCap) {
+      g_pool[ctx->device].push_back(ctx);
+      return QSB_OK;
+    }
+  }
+  destroy_now(ctx);
   return QSB_OK;
 }
 
@@ -248,11 +314,36 @@ int qsb_ctx_launches(qsb_ctx* ctx, uint64_t* out) {
   return QSB_OK;
 }
 
-int qsb_alloc(qsb_ctx* ctx, uint64_t bytes, void** dptr) {
-  if (!ctx || !dptr) return invalid("null argument");
-  QSB_CUDA(cudaSetDevice(ctx->device));
-  *dptr = nullptr;
+}  // extern "C"
+
+// Device memory.  cudaMalloc / cudaFree cost milliseconds each (cudaFree synchronises
+// the device) -- per handle that is more than a small register's whole E+grad -- so
+// buffers up to 1 GiB come from the device's stream-ordered pool (cudaMallocAsync on
+// the context's stream, cudaFreeAsync back to it, up to 8 GiB kept cached); larger ones
+// and CUDA-IPC-exported shard buffers (qsb_alloc_ipc) use cudaMalloc.
+namespace {
+constexpr uint64_t kPooledMax = 1ull << 30;
+constexpr uint64_t kPoolKeep = 8ull << 30;
+std::mutex g_alloc_mu;
+std::unordered_set<void*> g_pooled;
+qsb::PerDevice<cudaError_t> g_poolcfg;
+
+bool pool_enabled() {
+  const char* e = getenv("QSB_NO_MEMPOOL");
+  return !(e && atoi(e));
+}
+
+int plain_alloc(qsb_ctx* ctx, uint64_t bytes, void** dptr) {
   cudaError_t e = cudaMalloc(dptr, bytes ? bytes : 16);
+  if (e == cudaErrorMemoryAllocation) {  // cached pool memory may be in the way: trim, retry
+    cudaGetLastError();
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) {
+      cudaDeviceSynchronize();
+      cudaMemPoolTrimTo(pool, 0);
+    }
+    e = cudaMalloc(dptr, bytes ? bytes : 16);
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     set_error("device allocation of %llu bytes failed (%s)", (unsigned long long)bytes, cudaGetErrorString(e));
@@ -260,13 +351,55 @@ int qsb_alloc(qsb_ctx* ctx, uint64_t bytes, void** dptr) {
   }
   return QSB_OK;
 }
+}  // namespace
+
+extern "C" {
+
+int qsb_alloc(qsb_ctx* ctx, uint64_t bytes, void** dptr) {
+  if (!ctx || !dptr) return invalid("null argument");
+  QSB_CUDA(cudaSetDevice(ctx->device));
+  *dptr = nullptr;
+  if (bytes <= kPooledMax && pool_enabled()) {
+    const cudaError_t cfg = g_poolcfg.get(ctx->device, [&] {
+      cudaMemPool_t pool;
+      cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, ctx->device);
+      uint64_t keep = kPoolKeep;
+      if (e == cudaSuccess) e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      return e;
+    });
+    if (cfg == cudaSuccess) {
+      cudaError_t e = cudaMallocAsync(dptr, bytes ? bytes : 16, ctx->stream);
+      if (e == cudaSuccess) {
+        std::lock_guard<std::mutex> g(g_alloc_mu);
+        g_pooled.insert(*dptr);
+        return QSB_OK;
+      }
+      cudaGetLastError();  // fall through to cudaMalloc
+      *dptr = nullptr;
+    }
+  }
+  return plain_alloc(ctx, bytes, dptr);
+}
+
+int qsb_alloc_ipc(qsb_ctx* ctx, uint64_t bytes, void** dptr) {
+  if (!ctx || !dptr) return invalid("null argument");
+  QSB_CUDA(cudaSetDevice(ctx->device));
+  *dptr = nullptr;
+  return plain_alloc(ctx, bytes, dptr);
+}
 
 // ctx may be NULL (its context already destroyed): cudaFree synchronises the
 // device implicitly, so queued work on any stream has finished with the buffer.
 int qsb_free(qsb_ctx* ctx, void* dptr) {
   if (!dptr) return QSB_OK;
+  bool pooled;
+  {
+    std::lock_guard<std::mutex> g(g_alloc_mu);
+    pooled = g_pooled.erase(dptr) > 0;
+  }
   if (ctx) QSB_CUDA(cudaSetDevice(ctx->device));
-  QSB_CUDA(cudaFree(dptr));
+  if (pooled && ctx) QSB_CUDA(cudaFreeAsync(dptr, ctx->stream));  // stream-ordered after its uses
+  else QSB_CUDA(cudaFree(dptr));
   return QSB_OK;
 }
 

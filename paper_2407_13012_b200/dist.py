@@ -520,14 +520,15 @@ class ShardedHandle:
                 self.tables[layout][k] = vals
                 lo, hi = min(lo, mn.value), max(hi, mx.value)
         self.min_value, self.max_value = self._minmax(lo, hi)
-        self.ket = [DeviceArray(dctx, N_l, np.complex128) for _ in self.ranks]
-        self.bra = [DeviceArray(dctx, N_l, np.complex128) for _ in self.ranks]
-        self.scratch = [DeviceArray(dctx, N_l, np.complex128) for _ in self.ranks]
+        # statevector buffers: plain cudaMalloc memory (exportable to peer processes)
+        self.ket = [DeviceArray(dctx, N_l, np.complex128, ipc=True) for _ in self.ranks]
+        self.bra = [DeviceArray(dctx, N_l, np.complex128, ipc=True) for _ in self.ranks]
+        self.scratch = [DeviceArray(dctx, N_l, np.complex128, ipc=True) for _ in self.ranks]
         # a fused swap of a bra/ket visit needs a second spare (up front for P2P, whose
         # buffers are exported once; lazily for virtual shards)
         self.scratch_bra = None
         if exchanger.fused and not isinstance(exchanger, VirtualExchanger):
-            self.scratch_bra = [DeviceArray(dctx, N_l, np.complex128) for _ in self.ranks]
+            self.scratch_bra = [DeviceArray(dctx, N_l, np.complex128, ipc=True) for _ in self.ranks]
         self.layout = 0
         self._plus_pending = False  # the ket is |+> by contract but not written (after a gradient)
         exchanger.setup(self)
