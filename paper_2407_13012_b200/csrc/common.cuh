@@ -63,6 +63,10 @@ struct qsb_ctx {
   // reusable device buffer for small uploads (LUTs, terms)
   void* d_small = nullptr;
   uint64_t small_bytes = 0;
+  // forward checkpoints of the adjoint walk (spare HBM, fused.cu run_chain): kept between
+  // calls, released when the context is destroyed or an allocation needs the memory
+  std::vector<void*> ck;
+  uint64_t ck_bytes = 0;
   // live per-kernel profiling (qsb_prof_begin/end): CUDA events around each sweep
   bool prof = false;
   struct ProfRec {
@@ -111,6 +115,10 @@ int ensure_scratch(qsb_ctx* ctx, uint64_t bytes);
 int ensure_small(qsb_ctx* ctx, uint64_t bytes);
 int ensure_sample_scratch(qsb_ctx* ctx, uint64_t bytes);
 int ensure_shot_scratch(qsb_ctx* ctx, uint64_t bytes);
+// up to `want` device buffers of `bytes` each for forward checkpoints, as many as fit in
+// free HBM above a margin (QSB_CKPT_MARGIN_GB, default 8; QSB_NO_CKPT=1: none)
+int ensure_checkpoints(qsb_ctx* ctx, uint64_t bytes, int want, std::vector<double2*>& out);
+void release_checkpoints(qsb_ctx* ctx);
 // build (cos, sin) of (sign * gamma * v) for v = vmin + k, k < nvals, with host libm
 // (the same values Python's math.cos/sin and numba give) and upload to t->d_lut.
 int upload_phase_lut(qsb_table* t, double ang_scale, double2 extra_scale, bool exact);

@@ -98,6 +98,62 @@ int ensure_small(qsb_ctx* ctx, uint64_t bytes) {
   return QSB_OK;
 }
 
+// Forward checkpoints.  Contexts holding them are registered so an allocation that runs
+// out of memory can take the memory back (release_all_checkpoints).
+namespace {
+std::mutex g_ck_mu;
+std::unordered_set<qsb_ctx*> g_ck_ctxs;
+}  // namespace
+
+void release_checkpoints(qsb_ctx* ctx) {
+  if (ctx->ck.empty()) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (void* p : ctx->ck) cudaFree(p);
+  ctx->ck.clear();
+  ctx->ck_bytes = 0;
+  std::lock_guard<std::mutex> g(g_ck_mu);
+  g_ck_ctxs.erase(ctx);
+}
+
+void release_all_checkpoints() {
+  std::vector<qsb_ctx*> all;
+  {
+    std::lock_guard<std::mutex> g(g_ck_mu);
+    all.assign(g_ck_ctxs.begin(), g_ck_ctxs.end());
+  }
+  for (qsb_ctx* c : all) release_checkpoints(c);
+}
+
+int ensure_checkpoints(qsb_ctx* ctx, uint64_t bytes, int want, std::vector<double2*>& out) {
+  out.clear();
+  const char* off = getenv("QSB_NO_CKPT");
+  if ((off && atoi(off)) || want <= 0) return QSB_OK;
+  if (ctx->ck_bytes != bytes) release_checkpoints(ctx);
+  if ((int)ctx->ck.size() < want) {
+    const char* m = getenv("QSB_CKPT_MARGIN_GB");
+    const uint64_t margin = (uint64_t)(m ? atof(m) : 8.0) << 30;
+    size_t fr = 0, tot = 0;
+    QSB_CUDA(cudaMemGetInfo(&fr, &tot));
+    while ((int)ctx->ck.size() < want && fr > margin + bytes) {
+      void* p = nullptr;
+      if (cudaMalloc(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        break;
+      }
+      ctx->ck.push_back(p);
+      fr -= bytes;
+    }
+    ctx->ck_bytes = ctx->ck.empty() ? 0 : bytes;
+    if (!ctx->ck.empty()) {
+      std::lock_guard<std::mutex> g(g_ck_mu);
+      g_ck_ctxs.insert(ctx);
+    }
+  }
+  for (int i = 0; i < want && i < (int)ctx->ck.size(); ++i) out.push_back((double2*)ctx->ck[i]);
+  return QSB_OK;
+}
+
 int prof_mark(qsb_ctx* ctx, cudaEvent_t* ev) {
   if (ctx->prof_used == ctx->prof_pool.size()) {
     cudaEvent_t e;
@@ -211,6 +267,7 @@ int qsb_ctx_destroy(qsb_ctx* ctx) {
   if (!ctx) return QSB_OK;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  release_checkpoints(ctx);
   // the sampler's scratch is sized by the largest state drawn (0.5 GB at n=30): release it
   if (ctx->d_sample) cudaFree(ctx->d_sample);
   if (ctx->d_shots) cudaFree(ctx->d_shots);
@@ -335,8 +392,9 @@ bool pool_enabled() {
 
 int plain_alloc(qsb_ctx* ctx, uint64_t bytes, void** dptr) {
   cudaError_t e = cudaMalloc(dptr, bytes ? bytes : 16);
-  if (e == cudaErrorMemoryAllocation) {  // cached pool memory may be in the way: trim, retry
+  if (e == cudaErrorMemoryAllocation) {  // checkpoints / cached pool memory may be in the way
     cudaGetLastError();
+    qsb::release_all_checkpoints();
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) {
       cudaDeviceSynchronize();

@@ -341,6 +341,13 @@ struct Runner {
   bool defer = false;
   double pend = 1.0;
   bool apply_now = false;  // set by the chain for the sweep that must store true values
+  // Forward checkpoints (spare HBM, value_and_grad): forward sweeps write their results to
+  // ck[] out of place, so the backward sweeps read the ket from them and never store it.
+  // in0 / out0: the v0 source / destination of the next sweep (nullptr: v0 in place).
+  std::vector<double2*> ck;
+  bool want_ck = false;  // run_chain asks the context for up to F checkpoints (spare HBM)
+  double2* in0 = nullptr;
+  double2* out0 = nullptr;
 
   int init(int total_sweeps_upper) {
     shapes = plan_sweeps(n);
@@ -398,14 +405,16 @@ struct Runner {
       const int pm = pair_mode();
       a.want_pair = ((nv == 1 && ((pm == 1 && mode == SM_PLAIN) || pm == 2)) || pm == 3) ? 1 : 0;
     }
-    a.v0 = v0;
+    a.v0 = in0 ? in0 : v0;
     a.v1 = v1;
+    a.o0 = out0;
+    in0 = out0 = nullptr;  // one sweep only
     set_table(a, t);
     // (a bridge always reads the table: bra = C * ket between its passes)
     const bool table_ops = (flags & kTableOps) || mode == SM_BRIDGE;
     a.cmode = (t && t->kind != 0 && table_ops) ? ((!sh.is_a && t->kind == 1) ? 2 : 1) : 0;
     if (!sh.is_a) {  // TMA boxes for the strided B tiles
-      QSB_TRY(encode_b_tile_map(&a.tm0, v0, st(), a.glo));
+      QSB_TRY(encode_b_tile_map(&a.tm0, a.v0, st(), a.glo));
       if (nv == 2) QSB_TRY(encode_b_tile_map(&a.tm1, v1, st(), a.glo));
       if (a.cmode) QSB_TRY(encode_b_cidx_map(&a.tmc, t->cidx, t->kind == 1 ? 1 : 2, st(), a.glo));
     }
@@ -561,16 +570,26 @@ std::vector<Visit> chain_visits(int n, const std::vector<SweepShape>& wins, int 
     const int hi = wins[w].is_a ? std::min(kSweepT, n) - 1 : wins[w].glo + 8;
     return ((hi >= 63 ? ~0ull : ((1ull << (hi + 1)) - 1)) & ~((1ull << lo) - 1));
   };
+  // forward layer i visits the windows ascending (i even) or descending (i odd), each
+  // gating the qubits its predecessors in the layer have not; backward layer i visits
+  // exactly forward layer i's (window, qubits) list in reverse, so every backward visit
+  // undoes one forward visit -- with overlapping windows (n < 30: the top B window slides
+  // down into the A window) a freshly computed descending partition would differ, and a
+  // bridge could not keep the ket it leaves unchanged, nor a backward sweep read its ket
+  // from a forward checkpoint
   auto layer = [&](bool b, int i) {
-    const bool ascending = b ? (i % 2 == 1) : (i % 2 == 0);
+    const bool ascending = i % 2 == 0;
     uint64_t covered = 0;
+    std::vector<Visit> fl;
     for (int k = 0; k < K; ++k) {
       const int w = ascending ? k : K - 1 - k;
       const uint64_t m = gate_mask(w) & ~covered;
       covered |= m;
       if (!m) continue;
-      out.push_back({b, i, w, __builtin_ctzll(m), 63 - __builtin_clzll(m)});
+      fl.push_back({b, i, w, __builtin_ctzll(m), 63 - __builtin_clzll(m)});
     }
+    if (b) std::reverse(fl.begin(), fl.end());
+    out.insert(out.end(), fl.begin(), fl.end());
   };
   if (fwd)
     for (int i = 0; i < p; ++i) layer(false, i);
@@ -613,9 +632,45 @@ int run_chain(Runner& R, double2* ket, double2* bra, int p, const double* gammas
     return 3;
   };
 
+  // job kinds in launch order (0 forward, 1 bridge, 2 backward): the checkpoint wiring
+  // needs F, the number of forward jobs, before the first launch
+  auto is_pair = [&](int u) { return merge && u + 1 < M && vis[u + 1].win == vis[u].win && boundary(u) != 0; };
+  int F = 0;
+  for (int u = 0; u < M;) {
+    const bool pr = is_pair(u);
+    if (pr ? boundary(u) == 1 : !vis[u].bwd) ++F;
+    u += pr ? 2 : 1;
+  }
+  // (merged chains only: there every layer boundary is a merged sweep, so forward and
+  // backward jobs cover the same gates AND phases and backward job j starts exactly
+  // where forward job F-1-j ended; an unmerged chain applies a backward layer's inverse
+  // phase at the start of the next sweep instead)
+  const bool ck_ok = R.want_ck && fwd && bwd && merge;
+  if (ck_ok) QSB_TRY(ensure_checkpoints(R.ctx, 16ull << R.st(), F, R.ck));
+  const int K = ck_ok ? std::min<int>((int)R.ck.size(), F) : 0;
+  if (K > 0) R.defer = false;  // checkpoints hold true values: no scale carried along the chain
+  int fj = 0, bj = 0;  // forward / backward jobs launched so far
+  // forward job k >= F-K writes checkpoint k-(F-K) (reading the previous one); the bridge
+  // and backward job j < K read the ket from checkpoint K-1-j and do not store it
+  auto wire = [&](int kind, uint32_t& f) {
+    if (K == 0) return;
+    if (kind == 0) {
+      const int c = fj - (F - K);
+      if (c >= 0) {
+        R.out0 = R.ck[c];
+        R.in0 = c > 0 ? R.ck[c - 1] : nullptr;
+      }
+    } else if (kind == 1) {
+      R.in0 = R.ck[K - 1];
+    } else if (bj < K) {
+      R.in0 = R.ck[K - 1 - bj];
+      f |= SF_KEEP_V0;
+    }
+  };
+
   for (int u = 0; u < M;) {
     const Visit& v = vis[u];
-    const bool pair = merge && u + 1 < M && vis[u + 1].win == v.win && boundary(u) != 0;
+    const bool pair = is_pair(u);
     int idx = -1;
     if (pair) {
       const Visit& w = vis[u + 1];
@@ -644,7 +699,11 @@ int run_chain(Runner& R, double2* ket, double2* bra, int p, const double* gammas
         ang = gammas[v.layer];
       }
       R.apply_now = (!bwd && u + 2 >= M) || (f & SF_KEEP_V0);  // true values where the chain needs them
+      const int jk = kind == 1 ? 0 : kind == 2 ? 1 : 2;
+      wire(jk, f);
       QSB_TRY(R.sweep_any(nv, mode, win_of(v), pass2, ket, bra, gate_of(v), gate_of(w), f, lut, ang, one, true, &idx));
+      if (jk == 0) ++fj;
+      if (jk == 2) ++bj;
       if (kind == 2 && want_value) contribs.push_back({idx, 0, 0, 0});
       if (v.bwd) contribs.push_back({idx, 2, 2, v.layer});
       if (kind == 3) contribs.push_back({idx, 1, 1, v.layer});
@@ -690,7 +749,10 @@ int run_chain(Runner& R, double2* ket, double2* bra, int p, const double* gammas
     if (post_dinner) f |= SF_POST_DINNER | SF_NO_STORE;
     if (v.bwd) f |= SF_XSUM;
     R.apply_now = !bwd && u == M - 1;
+    wire(v.bwd ? 2 : 0, f);
     QSB_TRY(R.sweep(v.bwd ? 2 : 1, win_of(v), ket, bra, gate_of(v), f, lut, ang, one, true, &idx));
+    if (v.bwd) ++bj;
+    else ++fj;
     if (post_expect) contribs.push_back({idx, 0, 0, 0});
     if (post_dinner) contribs.push_back({idx, 0, 1, v.layer});
     if (dinner_pre >= 0) contribs.push_back({idx, 1, 1, dinner_pre});
@@ -1026,6 +1088,7 @@ int qsb_value_and_grad(qsb_ctx* ctx, qsb_table* t, double* ket_, double* bra_, i
 
   Runner R{ctx, t, n, false};
   R.sym = !skip_forward && sym_ok(t, n, false);
+  R.want_ck = !skip_forward;
   QSB_TRY(R.init(upper_sweeps(n, p)));
   // LUTs: forward phases exp(-i g C) for layers 0..p-1, then inverse phases exp(+i g C) for layers 1..p-1
   std::vector<double> scales;

@@ -28,8 +28,9 @@ enum SweepFlags : uint32_t {
   SF_MID_DINNER = 1u << 10,  // NV=2 merged: slot1 += T*Im(conj(bra) ket) between the passes
   SF_MID_EXPECT = 1u << 11,  // bridge: slot0 += T*|ket|^2 between the passes
   SF_XSUM2 = 1u << 12,       // NV=2: slot3 += xsum over the second pass's qubits
-  SF_KEEP_V0 = 1u << 13,     // bridge: v0 is not stored -- pass 2 undoes pass 1 on the ket
-                             // (Rx(+2b) Rx(-2b) = 1), so HBM already holds its result
+  SF_KEEP_V0 = 1u << 13,     // NV=2: v0 (the ket) is not stored -- the bridge's pass 2 undoes
+                             // pass 1 (Rx(+2b) Rx(-2b) = 1), and a backward sweep whose ket
+                             // result the next sweep reads from a forward checkpoint
 };
 
 // A merged sweep applies two layers' gates to one window per HBM pass.  The chain
@@ -63,6 +64,8 @@ struct SweepArgs {
   CUtensorMap tmc;        // B shapes with table ops: 5-D box over the compact index (cmode)
   double2* v0;            // ket / the single vector
   double2* v1;            // bra (NV=2)
+  double2* o0;            // where v0's result goes (nullptr: in place; a forward checkpoint)
+  double2* o1;            // where v1's result goes (nullptr: in place)
   const void* cidx;       // compact table index (kind 1: u8, 2: u16)
   const double* table;    // fp64 table (kind 0)
   const double2* lut;     // pre-phase LUT (kind 1/2), includes any extra scale

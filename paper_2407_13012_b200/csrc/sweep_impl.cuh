@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
       for (int j = 0; j < NR; ++j) v[q][j] = make_double2(v[q][j].x * sc, v[q][j].y * sc);
     };
     auto store_vec = [&](int q) {
-      double2* dst = q == 0 ? a.v0 : a.v1;
+      double2* dst = q == 0 ? (a.o0 ? a.o0 : a.v0) : (a.o1 ? a.o1 : a.v1);  // out of place: a checkpoint
       if constexpr (MIR) {  // element (m, l): tile T at l, or tile ~T at 2047 - l
         const uint64_t t0 = tileT << 11, t1 = (tileT ^ a.tmask) << 11;
 #pragma unroll
@@ -863,7 +863,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     if (!(flags & SF_NO_STORE) && !tma_out) {
 #pragma unroll
       for (int q = Q0; q < Q1; ++q) {
-        if (q == 0 && MODE == SM_BRIDGE && (flags & SF_KEEP_V0)) continue;
+        if (q == 0 && (flags & SF_KEEP_V0)) continue;  // the ket's result is not stored
         store_vec(q);
       }
     }
@@ -872,11 +872,12 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
       if constexpr (TMAST) {
         if (tma_out && tid == 0) {
           const uint64_t tile = blockIdx.x + k * gridDim.x;
+          double2* ob = a.o0 ? a.o0 : a.v0;
           if constexpr (MIR) {
-            tma_store_1d(a.v0 + (tile << 11), xs_addr, kSlotBytes / 2);
-            tma_store_1d(a.v0 + ((tile ^ a.tmask) << 11), xs_addr + kSlotBytes / 2, kSlotBytes / 2);
+            tma_store_1d(ob + (tile << 11), xs_addr, kSlotBytes / 2);
+            tma_store_1d(ob + ((tile ^ a.tmask) << 11), xs_addr + kSlotBytes / 2, kSlotBytes / 2);
           } else if constexpr (IS_A) {
-            tma_store_1d(a.v0 + (tile << kSweepT), xs_addr, kSlotBytes);
+            tma_store_1d(ob + (tile << kSweepT), xs_addr, kSlotBytes);
           } else {
             const int lowbits = glo - 3;
             tma_store_5d(&a.tm0, (int)(tile & ((1ull << lowbits) - 1ull)), (int)(tile >> lowbits), xs_addr);
@@ -1046,7 +1047,8 @@ int launch_merged_f1(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
   // every flag a merged / bridge sweep of this kind can carry (run_chain, fused.cu)
   constexpr uint32_t M0 = SF_POST_SCALE | (MODE == SM_BRIDGE ? (uint32_t)(SF_MID_EXPECT | SF_XSUM2 | SF_KEEP_V0)
                                           : NV == 1 ? (uint32_t)SF_MID_PHASE
-                                                    : (uint32_t)(SF_XSUM | SF_MID_DINNER | SF_MID_PHASE | SF_XSUM2));
+                                                    : (uint32_t)(SF_XSUM | SF_MID_DINNER | SF_MID_PHASE | SF_XSUM2 |
+                                                                 SF_KEEP_V0));
   static_assert(!STG || (NV == 2 && MODE != SM_PLAIN), "the staggered schedule is a merged / bridge bra/ket sweep");
   constexpr uint32_t M = M0 | (STG ? kStagBit : 0u);
   if ((a.flags & ~M0) != 0) return invalid("internal: unexpected flags 0x%x for a merged sweep", a.flags);

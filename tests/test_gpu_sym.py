@@ -67,3 +67,35 @@ def test_reduced_batch_many():
         assert rel_err(np.concatenate([g.d_gammas, g.d_betas]), np.concatenate([dg, db])) <= 1e-10
     for h in hs:
         h.close()
+
+
+@pytest.mark.parametrize("n,p,sym", [(22, 3, True), (23, 2, False), (16, 4, True)])
+def test_forward_checkpoints(n, p, sym, monkeypatch):
+    """the adjoint walk with forward checkpoints in spare HBM (backward sweeps read the
+    ket from them and never store it) equals the in-place walk and the oracle"""
+    if sym:
+        poly = random_instance(1200 + n, n)
+    else:  # a QUBO-like table with linear terms: not flip-symmetric
+        rs = np.random.default_rng(n)
+        poly = qs.Polynomial(n, [((rs.random() - 0.5) * 4, 1 << i) for i in range(n)] +
+                             [((rs.random() - 0.5) * 4, (1 << i) | (1 << ((i + 3) % n))) for i in range(n)])
+    params = random_params(77 + n, p)
+    table = oracle.precompute_table(poly.weights, poly.masks, n)
+    e, dg, db = oracle.value_and_grad(table, n, params.gammas, params.betas)
+    h = qs.create_handle(poly, backend_name="b200")
+    v, g = qs.value_and_grad(h, params)  # checkpoints (default)
+    monkeypatch.setenv("QSB_NO_CKPT", "1")
+    v0, g0 = qs.value_and_grad(h, params)
+    monkeypatch.delenv("QSB_NO_CKPT")
+    monkeypatch.setenv("QSB_CKPT_MARGIN_GB", "170")  # no room: in place
+    v1, g1 = qs.value_and_grad(h, params)
+    got = np.concatenate([g.d_gammas, g.d_betas])
+    assert abs(v - min(max(e, table.min()), table.max())) <= 1e-10 * max(1.0, abs(e))
+    assert rel_err(got, np.concatenate([dg, db])) <= 1e-10
+    assert abs(v - v0) <= 1e-12 * max(1.0, abs(v))
+    assert rel_err(got, np.concatenate([g0.d_gammas, g0.d_betas])) <= 1e-12
+    assert rel_err(got, np.concatenate([g1.d_gammas, g1.d_betas])) <= 1e-12
+    # the ket is |+> by contract afterwards
+    plus = np.full(1 << n, 1.0 / np.sqrt(float(1 << n)))
+    assert np.max(np.abs(np.asarray(h.state.data) - plus)) <= 1e-12
+    h.close()

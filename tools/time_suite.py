@@ -60,7 +60,10 @@ for n in sorted(by_n):
         assert first == one
         bat = batch.value_and_grad_batch(hs, [params] * len(hs), threads=args.threads)
         t3 = time.perf_counter()
-        assert all(a == b for a, b in zip(one, bat)), n
+        for (va, ga), (vb, gb) in zip(one, bat):  # equal to rounding (checkpointed vs batched walk)
+            assert abs(va - vb) <= 1e-12 * max(1.0, abs(va)), n
+            assert max(abs(x - y) for x, y in zip(ga.d_betas + ga.d_gammas, gb.d_betas + gb.d_gammas)) <= \
+                1e-12 * max(1.0, max(abs(x) for x in ga.d_betas + ga.d_gammas)), n
         for h in hs:
             h.close()
         rows[n] = {"graphs": len(hs), "create_ms": 1e3 * (t1 - t0), "first_call_ms": 1e3 * (t2a - t1),
