@@ -91,6 +91,8 @@ struct qsb_table {
   void* cidx = nullptr;       // compact index table (owned)
   double2* d_lut = nullptr;   // phase LUT scratch (owned), up to 65536 entries
   std::vector<double> h_lutbuf;  // host staging
+  double2* d_flut = nullptr;  // angle LUTs of an fp64 table (fused.cu FloatLuts), grown on demand
+  uint64_t flut_cap = 0;      // entries
 };
 
 namespace qsb {

@@ -6,6 +6,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <memory>
 
 #include "sweep.cuh"
@@ -72,6 +73,20 @@ int prepare_luts(qsb_table* t, const std::vector<double>& ang_scales, const std:
 }  // namespace qsb
 
 namespace {
+
+// angle LUT of an fp64 table for one phase angle (see TvF64 in sweep_impl.cuh): m entries
+// e^{i ang (vmin + 256 k / S)}, then 256 entries e^{i ang j / S}
+__global__ void k_build_flut(double2* out, int m, double ang, double vmin, double S) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double sn, cn;
+  if (i < m) {
+    sincos(ang * (vmin + 256.0 * (double)i / S), &sn, &cn);
+    out[i] = make_double2(cn, sn);
+  } else if (i < m + 256) {
+    sincos(ang * ((double)(i - m) / S), &sn, &cn);
+    out[i] = make_double2(cn, sn);
+  }
+}
 
 // ------------------------------------------------------------------ planning
 struct SweepShape {
@@ -344,6 +359,53 @@ struct Runner {
   // Forward checkpoints (spare HBM, value_and_grad): forward sweeps write their results to
   // ck[] out of place, so the backward sweeps read the ket from them and never store it.
   // in0 / out0: the v0 source / destination of the next sweep (nullptr: v0 in place).
+  // angle LUTs of an fp64 table (fast mode), built lazily per angle into t->d_flut
+  struct FLut {
+    double ang, S;
+    int m;
+    uint64_t off;
+  };
+  std::vector<FLut> fluts;
+  uint64_t flut_used = 0;
+
+  const FLut* float_lut(double ang) {
+    if (!t || t->kind != 0 || exact) return nullptr;
+    const char* e = getenv("QSB_NO_FLUT");
+    if (e && atoi(e)) return nullptr;
+    for (const FLut& f : fluts)
+      if (f.ang == ang) return &f;
+    const double range = t->vmax - t->vmin;
+    if (!(range >= 0.0) || !std::isfinite(range)) return nullptr;
+    double S = 1.0;  // a power of two with |ang| / S <= 2^-9
+    while (fabs(ang) / S > 1.0 / 512.0) S *= 2.0;
+    const double mm = floor(range * S / 256.0) + 2.0;
+    if (mm > 65536.0) return nullptr;
+    const int m = (int)mm;
+    const uint64_t need = flut_used + (uint64_t)m + 256;
+    if (need > t->flut_cap) {  // grow, keeping this call's LUTs
+      const uint64_t cap = std::max<uint64_t>(need, 2 * t->flut_cap);
+      double2* nb = nullptr;
+      if (cudaMalloc(&nb, cap * sizeof(double2)) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+      }
+      if (t->d_flut) {
+        if (flut_used) cudaMemcpyAsync(nb, t->d_flut, flut_used * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream);
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(t->d_flut);
+      }
+      t->d_flut = nb;
+      t->flut_cap = cap;
+    }
+    const int total = m + 256;
+    k_build_flut<<<(total + 255) / 256, 256, 0, ctx->stream>>>(t->d_flut + flut_used, m, ang, t->vmin, S);
+    if (cudaGetLastError() != cudaSuccess) return nullptr;
+    ctx->launches++;
+    fluts.push_back({ang, S, m, flut_used});
+    flut_used = need;
+    return &fluts.back();
+  }
+
   std::vector<double2*> ck;
   bool want_ck = false;  // run_chain asks the context for up to F checkpoints (spare HBM)
   double2* in0 = nullptr;
@@ -418,11 +480,25 @@ struct Runner {
       if (nv == 2) QSB_TRY(encode_b_tile_map(&a.tm1, v1, st(), a.glo));
       if (a.cmode) QSB_TRY(encode_b_cidx_map(&a.tmc, t->cidx, t->kind == 1 ? 1 : 2, st(), a.glo));
     }
+    // merged / bridge sweeps over an fp64 table: TMA-stage each tile's table values for
+    // the mid ops (QSB_NO_FTAB=1: read them from HBM per element)
+    if (t && t->kind == 0 && t->values && !exact && mode != SM_PLAIN && !getenv("QSB_NO_FTAB")) {
+      a.ftab = 1;
+      if (!sh.is_a) QSB_TRY(encode_b_f64_map(&a.tmf, t->values, st(), a.glo));
+    }
     a.mirror = (sym && sh.is_a) ? 1 : 0;
     a.tmask = sym ? (1ull << (st() - 11)) - 1ull : 0ull;
     a.lut = lut;
     a.pre_ang = pre_ang;
     a.pre_extra = pre_extra;
+    if (t && t->kind == 0 && !exact && (flags & (SF_PRE_PHASE | SF_MID_PHASE))) {
+      if (const FLut* fl = float_lut(pre_ang)) {
+        a.flut = t->d_flut + fl->off;
+        a.fl_S = fl->S;
+        a.fl_xs = pre_ang / fl->S;
+        a.fl_m = fl->m;
+      }
+    }
     a.form = g1.form;
     a.ga = g1.ga;
     a.gb = g1.gb;

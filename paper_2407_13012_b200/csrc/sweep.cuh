@@ -62,6 +62,7 @@ struct PhaseMap {
 struct SweepArgs {
   CUtensorMap tm0, tm1;   // B shapes: 5-D TMA boxes over v0 / v1 (one 64 KB tile per load)
   CUtensorMap tmc;        // B shapes with table ops: 5-D box over the compact index (cmode)
+  CUtensorMap tmf;        // B shapes, staged fp64 table (ftab): 5-D box over the fp64 table
   double2* v0;            // ket / the single vector
   double2* v1;            // bra (NV=2)
   double2* o0;            // where v0's result goes (nullptr: in place; a forward checkpoint)
@@ -70,6 +71,12 @@ struct SweepArgs {
   const double* table;    // fp64 table (kind 0)
   const double2* lut;     // pre-phase LUT (kind 1/2), includes any extra scale
   double pre_ang;         // kind 0: factor = extra * (cos(pre_ang*T), sin(pre_ang*T))
+  // kind 0, fast mode: angle LUT of pre_ang (nullptr: device sincos) -- fl_m entries
+  // e^{i pre_ang (vmin + 256 k / fl_S)}, then 256 entries e^{i pre_ang j / fl_S}
+  const double2* flut;
+  double fl_S, fl_xs;     // scale S and pre_ang / S
+  int fl_m;
+  int ftab;               // merged / bridge sweep over an fp64 table: stage its tiles in smem
   double2 pre_extra;      // kind 0 extra complex scale
   double vmin;            // compact: T = vmin + idx
   double post_scale;
@@ -222,6 +229,8 @@ int launch_sweep(qsb_ctx* ctx, int nv, bool exact, SweepArgs& a, unsigned* grid_
 int encode_b_tile_map(CUtensorMap* map, const double2* base, int n, int glo);
 // 5-D box over the compact index (esz 1 or 2 bytes) for the same B tile
 int encode_b_cidx_map(CUtensorMap* map, const void* base, int esz, int n, int glo);
+// 5-D box over an fp64 table for the same B tile (4096 doubles in local-index order)
+int encode_b_f64_map(CUtensorMap* map, const double* base, int n, int glo);
 int sweep_grid(qsb_ctx* ctx, int nv, bool exact, uint64_t ntiles, unsigned* grid_out);
 
 }  // namespace qsb

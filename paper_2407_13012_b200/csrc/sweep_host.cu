@@ -150,4 +150,19 @@ int encode_b_cidx_map(CUtensorMap* map, const void* base, int esz, int n, int gl
   return QSB_OK;
 }
 
+int encode_b_f64_map(CUtensorMap* map, const double* base, int n, int glo) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return invalid("cuTensorMapEncodeTiled unavailable (driver too old?)");
+  if (glo < 3 || n - glo - 9 < 0) return invalid("internal: bad B table geometry n=%d glo=%d", n, glo);
+  const cuuint64_t dims[5] = {8, 1ull << (glo - 3), 32, 16, 1ull << (n - glo - 9)};
+  const cuuint64_t strides[4] = {64, (1ull << glo) * 8, (1ull << (glo + 5)) * 8, (1ull << (glo + 9)) * 8};
+  const cuuint32_t box[5] = {8, 1, 32, 16, 1};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return invalid("cuTensorMapEncodeTiled (fp64 table) failed (%d) n=%d glo=%d", (int)r, n, glo);
+  return QSB_OK;
+}
+
 }  // namespace qsb

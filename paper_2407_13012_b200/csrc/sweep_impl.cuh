@@ -50,7 +50,11 @@ constexpr uint32_t kCBytes = kTile * 2u;  // compact-index slot (u16 worst case)
 // conflict-free whatever the entries; larger LUTs (<= 256 entries) are stored once.
 constexpr int kLutRep = 80;
 constexpr uint32_t kLutBytes = kLutRep * 8 * 16;  // 10 KB (the 227 KB budget: ring + index ring + LUT + barriers)
-constexpr size_t kSmemBytes = (size_t)kRing * kSlotBytes + (size_t)kRing * kCBytes + kLutBytes + 64;
+constexpr size_t kSmemBytes = (size_t)kRing * kSlotBytes + (size_t)kRing * kCBytes + kLutBytes + 128;
+// an fp64 table tile (4096 doubles) staged for the mid ops of merged / bridge sweeps: one
+// slot over the compact-index ring and LUT area, which fp64 tables do not use
+constexpr uint32_t kTabBytes = kTile * 8u;
+static_assert(kTabBytes <= (size_t)kRing * kCBytes + kLutBytes, "fp64 table slot");
 static_assert(kSmemBytes <= 232448, "dynamic shared memory per block on sm_100");
 static_assert(256 * 16 <= kLutBytes, "a plain LUT of 256 entries must fit");
 
@@ -332,6 +336,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int s = 0; s < GR * kRing; ++s) mbar_init(bar_s + 8 * s, 1);
+    mbar_init(bar_s + 8 * 8, 1);  // the staged fp64 table tile (merged / bridge sweeps)
     if constexpr (STAG) {  // exchange barriers of the two vectors: one arrival per warp
       mbar_init(bar_s + 8 * 6, QSB_STAG_ARRIVE_ALL ? NT : 1u << W);
       mbar_init(bar_s + 8 * 7, QSB_STAG_ARRIVE_ALL ? NT : 1u << W);
@@ -413,6 +418,28 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     else asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(NT) : "memory");
   };
   auto wait_seq = [&](uint64_t s) { mbar_wait(seq_bar(s), (uint32_t)((s / (GR * kRing)) & 1)); };
+  // fp64 table tile of a merged / bridge sweep (a.ftab): loaded into one slot at the tile
+  // start (every thread has passed the previous tile's mid ops by then -- there is a CTA
+  // barrier between), waited for just before the mid ops; the slot overlays the
+  // compact-index ring (fp64 tables have none)
+  constexpr bool TSTG = GR == 1 && MODE != SM_PLAIN && !KSIN && !EXACT;
+  const bool tstage = TSTG && a.ftab;
+  const uint32_t tab_s = cring_s, tbar = bar_s + 8u * 8u;
+  const double* tsm = (const double*)cring;
+  auto issue_tab = [&](uint64_t tile) {
+    if (!tstage || threadIdx.x != 0) return;
+    fence_proxy_async();
+    mbar_expect_tx(tbar, kTabBytes);
+    if constexpr (MIR) {
+      tma_1d(tab_s, a.table + (tile << 11), kTabBytes / 2, tbar);
+      tma_1d(tab_s + kTabBytes / 2, a.table + ((tile ^ a.tmask) << 11), kTabBytes / 2, tbar);
+    } else if constexpr (IS_A) {
+      tma_1d(tab_s, a.table + (tile << kSweepT), kTabBytes, tbar);
+    } else {
+      const int lowbits = glo - 3;
+      tma_5d(tab_s, &a.tmf, (int)(tile & ((1ull << lowbits) - 1ull)), (int)(tile >> lowbits), tbar);
+    }
+  };
 
   double acc0 = 0.0, acc0b = 0.0, acc1 = 0.0, acc1b = 0.0, acc2 = 0.0, acc3 = 0.0;
   uint32_t fph[2] = {0u, 0u};  // STAG: phase parity of the two exchange barriers
@@ -440,6 +467,8 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
    if (k < my_tiles) {
     const uint64_t tileT = blockIdx.x + k * gridDim.x;
     const uint64_t base = tile_base(a, tileT);
+    issue_tab(tileT);
+    const uint32_t tpar = (uint32_t)(((k - (uint64_t)grp) / GR) & 1u);  // this tile's phase of tbar
     // table views: position of local element l in the smem index tile (the natural
     // layout) and its stored index (mirror: element (1, l) is stored at 2047 - l of ~T)
     auto tl = [&](uint32_t l) -> uint32_t { return nat(l); };
@@ -484,15 +513,52 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     }
 
     // ---------------------------------------------------------------- table views
-    struct TvF64 {  // f64 table from HBM, device sincos
+    struct TvF64 {  // f64 table from HBM: device sincos, or (fast mode) the angle LUT
       const SweepArgs& a;
       __device__ double val(uint32_t, uint64_t g) const { return a.table[g]; }
       __device__ double2 phase(uint32_t, uint64_t g) const {
-        double sn, cn;
-        sincos(a.pre_ang * a.table[g], &sn, &cn);
-        double2 f = make_double2(cn, sn);
+        double2 f;
+        if (!EXACT && a.flut) {
+          // e^{i ang T} = LUT1[k >> 8] * LUT2[k & 255] * e^{i x}: k = floor((T - vmin) S),
+          // x = ang (T - vmin - k / S), |x| <= 2^-9 (S is chosen per angle), Taylor to
+          // x^4 / x^5 (next terms < 2e-19): a few FMAs and two L1-cached loads instead of
+          // a full double-precision sincos per amplitude
+          const double u = (a.table[g] - a.vmin) * a.fl_S;
+          const double fu = floor(u);
+          const int k = (int)fu;
+          const double x = a.fl_xs * (u - fu), x2 = x * x;
+          const double c = fma(x2, fma(x2, 1.0 / 24.0, -0.5), 1.0);
+          const double sn = x * fma(x2, fma(x2, 1.0 / 120.0, -1.0 / 6.0), 1.0);
+          f = cmul_fast(cmul_fast(__ldg(&a.flut[k >> 8]), __ldg(&a.flut[a.fl_m + (k & 255)])), make_double2(c, sn));
+        } else {
+          double sn, cn;
+          sincos(a.pre_ang * a.table[g], &sn, &cn);
+          f = make_double2(cn, sn);
+        }
         if constexpr (!EXACT) f = cmul_fast(f, a.pre_extra);
         return f;
+      }
+    };
+    struct TvF64S {  // the staged fp64 tile (natural positions, tl-mapped by the caller)
+      const SweepArgs& a;
+      const double* tsm;
+      __device__ double val(uint32_t l, uint64_t) const { return tsm[l]; }
+      __device__ double2 phase(uint32_t l, uint64_t) const {
+        double2 f;
+        if (a.flut) {  // see TvF64
+          const double u = (tsm[l] - a.vmin) * a.fl_S;
+          const double fu = floor(u);
+          const int k = (int)fu;
+          const double x = a.fl_xs * (u - fu), x2 = x * x;
+          const double c = fma(x2, fma(x2, 1.0 / 24.0, -0.5), 1.0);
+          const double sn = x * fma(x2, fma(x2, 1.0 / 120.0, -1.0 / 6.0), 1.0);
+          f = cmul_fast(cmul_fast(__ldg(&a.flut[k >> 8]), __ldg(&a.flut[a.fl_m + (k & 255)])), make_double2(c, sn));
+        } else {
+          double sn, cn;
+          sincos(a.pre_ang * tsm[l], &sn, &cn);
+          f = make_double2(cn, sn);
+        }
+        return cmul_fast(f, a.pre_extra);
       }
     };
     // LUT slot of entry c: replicated (8c + lane%8) or plain (c)
@@ -528,6 +594,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
         if (cmode == 2) fn(TvU8Rows{a, cs, slut, tb8, lrep, lq});
         else if (a.kind == 1) fn(TvU8{a, cs, slut, lrep, lq});
         else if (a.kind == 2) fn(TvU16{a, (const uint16_t*)cs});
+        else if (tstage) fn(TvF64S{a, tsm});
         else fn(TvF64{a});
       }
     };
@@ -640,6 +707,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     // (local base lbm)
     auto mid_ops = [&](uint32_t lbm) {
       constexpr int RM = shape_phase(SH, NP - 1).reg_l;
+      if (tstage) mbar_wait(tbar, tpar);
       with_table([&](auto tv) {
 #pragma unroll
         for (int j = 0; j < NR; ++j) {

@@ -268,6 +268,7 @@ int qsb_table_destroy(qsb_table* t) {
   if (!t) return QSB_OK;
   if (t->cidx) cudaFree(t->cidx);
   if (t->d_lut) cudaFree(t->d_lut);
+  if (t->d_flut) cudaFree(t->d_flut);
   delete t;
   return QSB_OK;
 }
