@@ -135,6 +135,13 @@ int sweep_family(int nv, int mode, bool is_a) {
     if (!e2) return is_a ? 4 : 3;
     return atoi(e2) == 3 ? 3 : 4;
   }
+  if (merged && !is_a) {  // QSB_SWEEP_R1MB: B windows only (A/B runs that keep the Z2 mirror A family)
+    const char* eb = getenv("QSB_SWEEP_R1MB");
+    if (eb) {
+      const int r = atoi(eb);
+      return (r == 5 || r == 6) ? r : 4;
+    }
+  }
   const char* e = getenv(merged ? "QSB_SWEEP_R1M" : (nv == 1 ? "QSB_SWEEP_R1" : "QSB_SWEEP_R2"));
   if (!e) return nv == 2 ? 4 : merged ? (is_a ? 4 : 5) : (is_a ? 6 : 4);
   int r = atoi(e);
