@@ -143,7 +143,9 @@ int sweep_family(int nv, int mode, bool is_a) {
     }
   }
   const char* e = getenv(merged ? "QSB_SWEEP_R1M" : (nv == 1 ? "QSB_SWEEP_R1" : "QSB_SWEEP_R2"));
-  if (!e) return nv == 2 ? 4 : merged ? (is_a ? 4 : 5) : (is_a ? 6 : 4);
+  // (round 2, Z2-reduced chain: merged single-vector B sweeps on two R=5 warp groups,
+  // 13.4 ms per C3 step vs 14.0 for R=4 and 16.5 for one R=5 group)
+  if (!e) return nv == 2 ? 4 : merged ? (is_a ? 4 : 6) : (is_a ? 6 : 4);
   int r = atoi(e);
   if (merged) return (r == 5 || r == 6) ? r : 4;
   if (nv == 2 && r >= 5) r = 4;  // two vectors of 32 amplitudes do not fit in registers
