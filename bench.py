@@ -604,6 +604,17 @@ def run_b200(args, rank: int, world: int, dist) -> None:
     h2d1, d2h1 = dev.xfer()
     wall_ms = (wall1 - wall0) * 1e3
 
+    # the same step with random angles (conftest.random_params(1, p): no beta = 0 layer, both
+    # factored gate forms) -- SURVEY.md §8(d) asks for ramp AND random parameters
+    other_kind = "random" if args.params == "ramp" else "ramp"
+    _, params_other = workload(args.n, args.p, other_kind)
+    qs.value_and_grad(h, params_other)
+    dev.sync()
+    dev.timer_start()
+    for _ in range(max(3, args.steps // 4)):
+        qs.value_and_grad(h, params_other)
+    other_ms = dev.timer_stop() / max(3, args.steps // 4)
+
     # forward-only layers/s (the reference's simulate)
     dev.sync()
     dev.timer_start()
@@ -661,6 +672,7 @@ def run_b200(args, rank: int, world: int, dist) -> None:
         "grad_norm_inf": max(abs(x) for x in list(grad.d_gammas) + list(grad.d_betas)),
         "layers_per_s": world * layers_per_s,
         "simulate_ms": sim_ms / args.steps,
+        f"{other_kind}_params_ms_per_step": other_ms,
         "precompute_s": precompute_s,
         "sampling": {"shots": args.shots, "device_ms": sample_ms, "wall_ms": sample_wall_ms,
                      "best_cost": best[1], "how": "qs.draw(handle, shots, seed=1) after simulate (C3)"},
@@ -684,6 +696,14 @@ def run_b200(args, rank: int, world: int, dist) -> None:
         },
         "sweeps_share_of_step": total_sweep_ms / ms,
         "step_hbm_gbs": all_bytes / (ms * 1e-3) / 1e9,
+        # the whole step against the copy peak: on the bytes the step actually moves, and
+        # on SURVEY.md §8(d)'s full-vector one-pass-per-window model (which the Z2
+        # reduction, merged sweeps and checkpoints undercut -- hence > 1)
+        "step_roofline": {
+            "bytes_per_step": all_bytes / args.steps,
+            "own_bytes_frac": all_bytes / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+            "survey_model_frac": survey_model(args.n, args.p, ms / args.steps, peaks["hbm_gbs"])["effective_frac"],
+        },
         # SURVEY.md §8(d)'s byte model for value_and_grad (S = 3 sweeps per layer, one
         # pass per window per layer): [p(96S+16) - 16] N.  The window chain moves fewer
         # bytes (above); against the model's bytes the step runs at this effective rate,

@@ -87,6 +87,8 @@ typedef struct qsb_table qsb_table;
 /* ---------------------------------------------------------------- errors */
 const char* qsb_last_error(void);
 int qsb_abi_version(void);
+/* 1 when the library carries the A/B experiment sweep families (-DQSB_VARIANTS) */
+int qsb_has_variants(void);
 
 /* ------------------------------------------------------ device / context */
 int qsb_device_count(int* out);

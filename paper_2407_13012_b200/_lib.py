@@ -36,6 +36,7 @@ _dp = C.POINTER(C.c_double)
 _SIGS = {
     "qsb_last_error": [],
     "qsb_abi_version": [],
+    "qsb_has_variants": [],
     "qsb_device_count": [C.POINTER(_i32)],
     "qsb_ctx_create": [_i32, C.POINTER(_vp)],
     "qsb_ctx_destroy": [_vp],
@@ -103,7 +104,7 @@ _SIGS = {
     "qsb_fill_const": [_vp, _vp, _u64, _dbl, _dbl],
     "qsb_table_detach_values": [_vp],
 }
-_RESTYPES = {"qsb_last_error": C.c_char_p, "qsb_abi_version": _i32}
+_RESTYPES = {"qsb_last_error": C.c_char_p, "qsb_abi_version": _i32, "qsb_has_variants": _i32}
 
 # symbols declared in include/qsb.h (checked by the CPU test suite)
 HEADER_SYMBOLS = tuple(_SIGS)
@@ -135,6 +136,11 @@ def load():
             fn.restype = _RESTYPES.get(name, _i32)
         _lib = lib
         return lib
+
+
+def has_variants() -> bool:
+    """the library carries the A/B experiment sweep families (tools/build_variant.py)"""
+    return bool(load().qsb_has_variants())
 
 
 def last_error() -> str:

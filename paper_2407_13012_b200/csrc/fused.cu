@@ -135,6 +135,10 @@ int sweep_family(int nv, int mode, bool is_a) {
     if (!e2) return is_a ? 4 : 3;
     return atoi(e2) == 3 ? 3 : 4;
   }
+  if (!merged && nv == 1 && is_a) {  // QSB_SWEEP_R1A: plain single-vector A windows only (A/B runs)
+    const char* ea = getenv("QSB_SWEEP_R1A");
+    if (ea) return atoi(ea) == 4 ? 4 : 6;
+  }
   if (merged && !is_a) {  // QSB_SWEEP_R1MB: B windows only (A/B runs that keep the Z2 mirror A family)
     const char* eb = getenv("QSB_SWEEP_R1MB");
     if (eb) {

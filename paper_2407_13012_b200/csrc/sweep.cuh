@@ -232,5 +232,11 @@ int encode_b_cidx_map(CUtensorMap* map, const void* base, int esz, int n, int gl
 // 5-D box over an fp64 table for the same B tile (4096 doubles in local-index order)
 int encode_b_f64_map(CUtensorMap* map, const double* base, int n, int glo);
 int sweep_grid(qsb_ctx* ctx, int nv, bool exact, uint64_t ntiles, unsigned* grid_out);
+// the A/B experiment families (env knobs selecting non-default register families or the
+// lock-step schedules) are compiled only with -DQSB_VARIANTS (tools/build_variant.py)
+inline int variant_missing() {
+  return invalid("this sweep family is an A/B experiment variant: build it with "
+                 "`python tools/build_variant.py variants QSB_VARIANTS=1` and select it with QSB_LIB");
+}
 
 }  // namespace qsb

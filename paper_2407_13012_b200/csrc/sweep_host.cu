@@ -79,6 +79,18 @@ int launch_sweep(qsb_ctx* ctx, int nv, bool exact, SweepArgs& a, unsigned* gout)
   return r == 4 ? launch_sweep_nv2_r4(ctx, a, gout) : launch_sweep_nv2_r3(ctx, a, gout);
 }
 
+}  // namespace qsb
+
+extern "C" int qsb_has_variants(void) {
+#ifdef QSB_VARIANTS
+  return 1;
+#else
+  return 0;
+#endif
+}
+
+namespace qsb {
+
 int sweep_grid(qsb_ctx* ctx, int nv, bool exact, uint64_t ntiles, unsigned* g) {
   // every shape runs one persistent CTA per SM (the ring takes ~220 KB of smem)
   (void)nv;

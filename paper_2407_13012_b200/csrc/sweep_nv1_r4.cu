@@ -3,6 +3,6 @@
 
 namespace qsb {
 int launch_sweep_nv1_r4(qsb_ctx* ctx, SweepArgs& a, unsigned* g) {
-  return sweepk::launch_fast<1, SH_A2, SH_B2>(ctx, a, g);
+  return sweepk::launch_fast<1, SH_A2, SH_B2, 1, 0xffffffffu, true>(ctx, a, g);
 }
 }  // namespace qsb

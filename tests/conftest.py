@@ -33,6 +33,21 @@ def _have_gpu() -> bool:
 HAVE_GPU = _have_gpu()
 
 
+# env knobs that select the A/B experiment sweep families, compiled only into a
+# -DQSB_VARIANTS build (tools/build_variant.py); the product library omits them
+_VARIANT_ONLY = {"QSB_STAG": {"0"}, "QSB_STAGP": {"0", "1", "2"}, "QSB_SWEEP_R1M": {"5"}, "QSB_SWEEP_R1MB": {"5"},
+                 "QSB_SWEEP_R1": {"3", "5"}, "QSB_SWEEP_R2": {"3"}}
+
+
+def variant_available(env: dict) -> bool:
+    """True when the loaded library can run the sweep families `env` selects"""
+    from paper_2407_13012_b200 import _lib
+
+    if _lib.has_variants():
+        return True
+    return not any(env.get(k) in vals for k, vals in _VARIANT_ONLY.items())
+
+
 def pytest_collection_modifyitems(config, items):
     if HAVE_GPU:
         return

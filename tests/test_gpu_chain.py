@@ -10,7 +10,7 @@ import pytest
 
 import paper_2407_13012_b200 as qs
 
-from conftest import random_instance, random_params, rel_err
+from conftest import variant_available, random_instance, random_params, rel_err
 from oracle import oracle
 
 pytestmark = pytest.mark.gpu
@@ -97,6 +97,9 @@ def test_chain_register_families(n, p, fam, monkeypatch):
     """single-vector sweeps with 32 amplitudes per thread (R=5: B windows need one
     exchange per pass; family 6 = two independent warp groups per CTA) against the
     default R=4 family"""
+    env = {"r2m3": {"QSB_SWEEP_R2M": "3"}, "pair": {"QSB_PAIR": "2"}}.get(fam, {"QSB_SWEEP_R1M": fam, "QSB_SWEEP_R1": fam})
+    if not variant_available(env):
+        pytest.skip(f"{env}: an A/B experiment sweep family (build with tools/build_variant.py QSB_VARIANTS=1)")
     poly = random_instance(300 + n, n)
     params = params_wide(11 * n + p, p)
     ref = run(poly, params, monkeypatch, merge=True)

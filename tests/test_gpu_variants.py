@@ -15,7 +15,7 @@ import pytest
 
 import paper_2407_13012_b200 as qs
 
-from conftest import random_instance, rel_err
+from conftest import variant_available, random_instance, rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -62,6 +62,8 @@ def test_schedule_variants_agree(n, p, monkeypatch):
     try:
         v0, g0, psi0 = evaluate(h, params)
         for env in VARIANTS:
+            if not variant_available(env):  # an A/B experiment family not in this build
+                continue
             with monkeypatch.context() as m:
                 for k, val in env.items():
                     m.setenv(k, val)
