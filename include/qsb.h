@@ -83,6 +83,7 @@ typedef struct qsb_shard_visit {
 
 typedef struct qsb_ctx qsb_ctx;
 typedef struct qsb_table qsb_table;
+typedef struct qsb_nccl qsb_nccl; /* an NCCL communicator bound to a context (nccl.cu) */
 
 /* ---------------------------------------------------------------- errors */
 const char* qsb_last_error(void);
@@ -255,6 +256,18 @@ int qsb_sample_descend(qsb_ctx* ctx, qsb_table* t, const double* amps, int n_loc
  * stores cross NVLink; complete with qsb_device_sync + a host barrier). */
 int qsb_scatter_chunks(qsb_ctx* ctx, const double* src, uint64_t chunk_amps, int nchunks, void* const* dsts,
                        uint64_t dst_off_amps);
+/* Native NCCL transport of the same swap (no reference counterpart; SURVEY.md §8(e)
+ * "The collective", the non-P2P mode of dist.py TorchExchanger).  libnccl.so.2 is
+ * opened at run time; without it these return QSB_EINVAL with the reason.
+ * unique_id: 128 bytes (rank 0 creates it, the caller broadcasts it); init binds the
+ * communicator to ctx's device and stream; all_to_all: dst chunk c <- rank c's src
+ * chunk `rank` (chunk_amps complex128 amplitudes per chunk, nranks chunks), one NCCL
+ * group of send/recv pairs on the context stream (stream-ordered, no host sync). */
+int qsb_nccl_version(int* version);
+int qsb_nccl_unique_id(void* id);
+int qsb_nccl_init(qsb_ctx* ctx, const void* id, int nranks, int rank, qsb_nccl** out);
+int qsb_nccl_all_to_all(qsb_nccl* c, const double* src, double* dst, uint64_t chunk_amps);
+int qsb_nccl_destroy(qsb_nccl* c);
 /* amps[i] = re + i*im (a shard's part of |+> is 1/sqrt(2^n_global), fill_plus
  * numba_impl.py:40-44 for the whole register) */
 int qsb_fill_const(qsb_ctx* ctx, double* amps, uint64_t len, double re, double im);

@@ -103,6 +103,11 @@ _SIGS = {
     "qsb_ctx_last_half": [_vp, C.POINTER(_i32)],
     "qsb_fill_const": [_vp, _vp, _u64, _dbl, _dbl],
     "qsb_table_detach_values": [_vp],
+    "qsb_nccl_version": [C.POINTER(_i32)],
+    "qsb_nccl_unique_id": [_vp],
+    "qsb_nccl_init": [_vp, _vp, _i32, _i32, C.POINTER(_vp)],
+    "qsb_nccl_all_to_all": [_vp, _vp, _vp, _u64],
+    "qsb_nccl_destroy": [_vp],
 }
 _RESTYPES = {"qsb_last_error": C.c_char_p, "qsb_abi_version": _i32, "qsb_has_variants": _i32}
 

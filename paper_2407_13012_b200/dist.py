@@ -255,6 +255,43 @@ class VirtualExchanger:
     def setup(self, handle) -> None:
         pass
 
+    def _setup_nccl(self, handle, force: bool = False) -> None:
+        """libqsb's own NCCL communicator for the all-to-all swaps: rank 0's unique id is
+        broadcast, every rank initialises, and all agree (one all_reduce) -- any failure
+        leaves every rank on torch.distributed's all_to_all_single."""
+        import os
+
+        import torch
+
+        mode = os.environ.get("QSB_SHARD_NCCL", "native")  # native | torch | force (also over gloo: tests)
+        force = force or mode == "force"
+        if (self.cpu and not force) or mode == "torch":
+            return
+        self._ctx = handle.ctx.device.handle
+        uid = np.zeros(129, dtype=np.uint8)
+        if self.rank == 0:
+            try:
+                call("qsb_nccl_unique_id", uid.ctypes.data)
+                uid[128] = 1
+            except Exception:  # noqa: BLE001 -- decided collectively below
+                uid[128] = 0
+        t = torch.as_tensor(uid, device=self._tdev())
+        self.dist.broadcast(t, src=0)
+        uid = np.ascontiguousarray(t.cpu().numpy())
+        comm = C.c_void_p()
+        ok = int(uid[128] == 1)
+        if ok:
+            try:
+                call("qsb_nccl_init", self._ctx, uid.ctypes.data, self.G, self.rank, C.byref(comm))
+            except Exception:  # noqa: BLE001
+                ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=self._tdev())
+        self.dist.all_reduce(flag, op=self.dist.ReduceOp.MIN)
+        if int(flag.item()) == 1:
+            self._nccl = comm.value
+        elif comm.value:
+            call("qsb_nccl_destroy", comm.value)
+
     def targets(self, name: str, spare: list[DeviceArray]) -> list[int]:
         """where the fused swap store sends tile chunk c: shard c's spare buffer"""
         return [b.ptr for b in spare]
@@ -297,9 +334,12 @@ class TorchExchanger:
     that owns it after the swap (NVLink P2P stores overlapped with the sweep; no separate
     pass).  Swaps outside a fused visit (a draw after an odd number of layers, exact
     mode, shards below 21 local qubits) then run qsb_scatter_chunks into the same peer
-    buffers.  Without P2P the swap is an NCCL all-to-all after the A visit; with a gloo
-    process group (tests: two processes on one GPU) the host-side collectives run on CPU
-    tensors and the non-P2P swap is staged through host memory."""
+    buffers.  Without P2P the swap is an all-to-all after the A visit: libqsb's own NCCL
+    communicator (qsb_nccl_*, one group of send/recv pairs on the context stream, no host
+    sync) when libnccl loads, else torch.distributed's all_to_all_single
+    (QSB_SHARD_NCCL=torch forces it); with a gloo process group (tests: two processes on
+    one GPU) the host-side collectives run on CPU tensors and the non-P2P swap is staged
+    through host memory."""
 
     def __init__(self, g: int, dist, device: int, p2p: bool | None = None):
         import os
@@ -319,6 +359,7 @@ class TorchExchanger:
         self._parity: dict[str, int] = {}
         self._opened: list[int] = []
         self._ctx = None
+        self._nccl = None  # qsb_nccl communicator (non-P2P swaps over NCCL)
 
     def _tdev(self) -> str:
         return "cpu" if self.cpu else f"cuda:{self.device}"
@@ -332,6 +373,7 @@ class TorchExchanger:
         all_gather, opened with no collective in between, and the outcome agreed by
         one all_reduce."""
         if not self.fused:
+            self._setup_nccl(handle)
             return
         import torch
 
@@ -375,6 +417,44 @@ class TorchExchanger:
             self.close()
             self._peers, self._parity = {}, {}
             self.fused = False
+            self._setup_nccl(handle)
+
+    def _setup_nccl(self, handle, force: bool = False) -> None:
+        """libqsb's own NCCL communicator for the all-to-all swaps: rank 0's unique id is
+        broadcast, every rank initialises, and all agree (one all_reduce) -- any failure
+        leaves every rank on torch.distributed's all_to_all_single."""
+        import os
+
+        import torch
+
+        mode = os.environ.get("QSB_SHARD_NCCL", "native")  # native | torch | force (also over gloo: tests)
+        force = force or mode == "force"
+        if (self.cpu and not force) or mode == "torch":
+            return
+        self._ctx = handle.ctx.device.handle
+        uid = np.zeros(129, dtype=np.uint8)
+        if self.rank == 0:
+            try:
+                call("qsb_nccl_unique_id", uid.ctypes.data)
+                uid[128] = 1
+            except Exception:  # noqa: BLE001 -- decided collectively below
+                uid[128] = 0
+        t = torch.as_tensor(uid, device=self._tdev())
+        self.dist.broadcast(t, src=0)
+        uid = np.ascontiguousarray(t.cpu().numpy())
+        comm = C.c_void_p()
+        ok = int(uid[128] == 1)
+        if ok:
+            try:
+                call("qsb_nccl_init", self._ctx, uid.ctypes.data, self.G, self.rank, C.byref(comm))
+            except Exception:  # noqa: BLE001
+                ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=self._tdev())
+        self.dist.all_reduce(flag, op=self.dist.ReduceOp.MIN)
+        if int(flag.item()) == 1:
+            self._nccl = comm.value
+        elif comm.value:
+            call("qsb_nccl_destroy", comm.value)
 
     def targets(self, name: str, spare: list[DeviceArray]) -> list[int]:
         par = self._parity[name]
@@ -387,6 +467,12 @@ class TorchExchanger:
         live[0].ptr, spare[0].ptr = spare[0].ptr, live[0].ptr
 
     def close(self) -> None:
+        if self._nccl:
+            try:
+                call("qsb_nccl_destroy", self._nccl)
+            except Exception:  # noqa: BLE001 -- best effort at teardown
+                pass
+            self._nccl = None
         for p_ in self._opened:
             try:
                 call("qsb_ipc_close", self._ctx, p_)
@@ -442,7 +528,9 @@ class TorchExchanger:
                  self.rank * chunk)
             self.commit(name, live, spare)
             return
-        if self.cpu:  # gloo stand-in: D2H, all-to-all of host tensors, H2D into the spare
+        if self._nccl:  # stream-ordered on the context stream: no host sync
+            call("qsb_nccl_all_to_all", self._nccl, v.ptr, s.ptr, chunk)
+        elif self.cpu:  # gloo stand-in: D2H, all-to-all of host tensors, H2D into the spare
             host = torch.from_numpy(v.to_host().view(np.float64)).view(self.G, -1)
             recv = torch.empty_like(host)
             self.dist.all_to_all_single(recv, host)

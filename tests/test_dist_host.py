@@ -261,3 +261,73 @@ def test_torch_exchanger_staged_swap_over_gloo():
 
 def test_p2p_setup_failure_on_one_rank_falls_back_everywhere():
     assert _spawn(_p2p_setup_worker, lambda r: ()) == {0: False, 1: False}
+
+
+def _nccl_setup_worker(rank, world, port, fail_rank, q):
+    """libqsb's NCCL communicator setup (TorchExchanger._setup_nccl) with the library
+    calls faked: rank 0's unique id is broadcast, every rank initialises, and one
+    all_reduce decides -- a rank whose init fails makes every rank stay on torch's
+    all-to-all (and the ranks that did initialise destroy their communicators)"""
+    import ctypes as C
+
+    import torch.distributed as tdist
+
+    from paper_2407_13012_b200 import _lib
+
+    tdist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    destroyed = []
+    seen_id = []
+    try:
+        def fake_call(name, *args):
+            if name == "qsb_nccl_unique_id":
+                C.memmove(args[0], bytes(range(7, 135)), 128)
+            elif name == "qsb_nccl_init":
+                seen_id.append(C.string_at(args[1], 128) == bytes(range(7, 135)))
+                if rank == fail_rank:
+                    raise _lib.ContractViolation("ncclCommInitRank: no")
+                args[4]._obj.value = 4096 + rank
+            elif name == "qsb_nccl_destroy":
+                destroyed.append(args[0])
+
+        dist.call = fake_call
+
+        class _Dev:
+            handle = None
+
+        class _Ctx:
+            device = _Dev()
+
+        class _H:
+            ctx = _Ctx()
+
+        ex = dist.TorchExchanger(1, tdist, 0, p2p=False)
+        ex._setup_nccl(_H(), force=True)
+        q.put((rank, (ex._nccl, destroyed, seen_id == [True])))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_native_nccl_setup_agrees_across_ranks():
+    assert _spawn(_nccl_setup_worker, lambda r: (-1,)) == {0: (4096, [], True), 1: (4097, [], True)}
+    assert _spawn(_nccl_setup_worker, lambda r: (1,)) == {0: (None, [4096], True), 1: (None, [], True)}
+
+
+def test_nccl_library_is_reachable():
+    """libqsb opens libnccl.so.2 at run time (the copy torch loaded): version and a
+    unique id work without a GPU; bad arguments are contract violations"""
+    import ctypes as C
+
+    import torch  # noqa: F401  (loads torch's NCCL first, as in a real run)
+
+    from paper_2407_13012_b200 import _lib
+
+    v = C.c_int32()
+    _lib.call("qsb_nccl_version", C.byref(v))
+    assert v.value >= 22700
+    uid = np.zeros(128, dtype=np.uint8)
+    _lib.call("qsb_nccl_unique_id", uid.ctypes.data)
+    assert uid.any()
+    with pytest.raises(_lib.ContractViolation):
+        _lib.call("qsb_nccl_init", None, uid.ctypes.data, 2, 0, C.byref(C.c_void_p()))
+    with pytest.raises(_lib.ContractViolation):
+        _lib.call("qsb_nccl_all_to_all", None, None, None, 0)

@@ -115,13 +115,14 @@ def test_sharded_window_chain(n, g, p, monkeypatch):
     assert rel_err(st1, st0) <= 1e-12
 
 
-@pytest.mark.parametrize("mode", ["p2p", "staged"])
+@pytest.mark.parametrize("mode", ["p2p", "staged", "nccl"])
 @pytest.mark.parametrize("n,p", [(22, 3), (16, 3)])
 def test_two_process_sharded(tmp_path, mode, n, p):
     """Two processes, one shard each (both on the one GPU here), for both transports
     of dist.TorchExchanger: "p2p" (qubit swap fused into the A visit's stores through
-    CUDA IPC; standalone swaps by the peer chunk scatter) and "staged" (the all-to-all
-    branch, host-staged over gloo).  n=22: the window chain (n_l = 21); n=16: the
+    CUDA IPC; standalone swaps by the peer chunk scatter), "staged" (the all-to-all
+    branch, host-staged over gloo) and "nccl" (the all-to-all on libqsb's own NCCL
+    communicator; host collectives still over gloo).  n=22: the window chain (n_l = 21); n=16: the
     per-position schedule (n_l < 21: every swap standalone).  Fast and exact
     value_and_grad, a draw after an odd number of layers (layout B -> swap back) and a
     draw after a gradient (ket |+> by contract) equal the single-process virtual-shard
@@ -131,13 +132,15 @@ def test_two_process_sharded(tmp_path, mode, n, p):
     import sys
 
     out = tmp_path / "res.npz"
-    port = 29531 + (n % 7) * 2 + (mode == "p2p")
+    port = 29531 + (n % 7) * 3 + ["staged", "p2p", "nccl"].index(mode)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={port}",
            os.path.join(os.path.dirname(__file__), "mp_shard_worker.py"), str(out), str(n), str(p), mode]
     res = subprocess.run(cmd, env=dict(os.environ), capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stderr[-3000:]
     got = np.load(out)
+    if mode == "nccl" and not int(got["native"]):
+        pytest.skip("NCCL would not initialise two ranks on one GPU (both fell back to the staged swap)")
     assert int(got["fused"]) == (1 if mode == "p2p" else 0)
     assert int(got["layout"]) == p % 2  # one swap per layer: odd p ends in layout B
     poly = random_instance(70 + n, n)
@@ -186,3 +189,33 @@ def test_sharded_chain_float_table_and_sampling():
     idx, cost = oracle.sample(state, table, 5000, 3)
     assert np.array_equal(ss.indices, idx) and np.array_equal(ss.costs, cost)
     sh.close()
+
+
+def test_native_nccl_all_to_all_single_rank():
+    """libqsb's NCCL transport on the GPU, one rank: the group of send/recv pairs on
+    the context stream moves the chunk, stream-ordered after the H2D and before the D2H
+    (two ranks: test_two_process_sharded's "nccl" mode)"""
+    import ctypes as C
+
+    import torch  # noqa: F401  (torch's NCCL is the one libqsb opens)
+
+    from paper_2407_13012_b200 import _lib
+    from paper_2407_13012_b200._lib import DeviceArray, DeviceContext, call
+
+    dctx = DeviceContext(0)
+    rs = np.random.default_rng(4)
+    x = rs.standard_normal(1 << 16) + 1j * rs.standard_normal(1 << 16)
+    src = DeviceArray(dctx, len(x), np.complex128)
+    dst = DeviceArray(dctx, len(x), np.complex128)
+    src.from_host(x)
+    uid = np.zeros(128, dtype=np.uint8)
+    call("qsb_nccl_unique_id", uid.ctypes.data)
+    comm = C.c_void_p()
+    call("qsb_nccl_init", dctx.handle, uid.ctypes.data, 1, 0, C.byref(comm))
+    try:
+        call("qsb_nccl_all_to_all", comm, src.ptr, dst.ptr, len(x))
+        assert np.array_equal(dst.to_host(), x)
+    finally:
+        call("qsb_nccl_destroy", comm)
+    with pytest.raises(_lib.ContractViolation):
+        call("qsb_nccl_init", dctx.handle, uid.ctypes.data, 1, 1, C.byref(C.c_void_p()))
