@@ -19,6 +19,13 @@ for chain in ("1", "0"):
         v, dg, db = sh.value_and_grad(params)
     sh.ctx.device.sync()
     dt = (time.perf_counter() - t0) / 3
+    dev = sh.ctx.device
+    dev.prof_begin()
+    sh.value_and_grad(params)
+    prof = dev.prof_end()
+    dev.sync()
+    kinds = "  ".join(f"{k}={v[1]:.1f}ms/{int(v[0])}x/{v[2] / max(v[1], 1e-9) / 1e6:.0f}GB/s"
+                      for k, v in sorted(prof.items()))
     print(f"n={n} g={g} p={p} {'window chain (fused swap)' if chain == '1' else 'per-position schedule + copy swap'}: "
-          f"{1e3 * dt:.1f} ms per E+grad (all {1 << g} shards on one GPU)  E={v:.12f}")
+          f"{1e3 * dt:.1f} ms per E+grad (all {1 << g} shards on one GPU)  E={v:.12f}\n    {kinds}")
 sh.close()
