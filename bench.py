@@ -543,14 +543,21 @@ def small_configs() -> dict:
     }
     h1.close()
     g2 = qs.maxcut_polynomial(qs.erdos_renyi(24, 0.5, seed=1))
-    t0 = time.perf_counter()
-    h2 = qs.create_handle(g2, backend_name="b200")
-    h2.ctx.synchronize()
-    pre = 1e3 * (time.perf_counter() - t0)
+    # create_handle twice: the first call grows the stream-ordered memory pool for this
+    # size (cold), the second is the steady-state table build + |+> fill (warm)
+    creates = []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        h2 = qs.create_handle(g2, backend_name="b200")
+        h2.ctx.synchronize()
+        creates.append(1e3 * (time.perf_counter() - t0))
+        if len(creates) == 1:
+            h2.close()
     p2 = qs.linear_ramp_params(4)
     qs.value_and_grad(h2, p2)
     out["C2_er24_p4"] = {
-        "precompute_ms": pre,
+        "precompute_ms": creates[1],
+        "create_handle_cold_ms": creates[0],
         "gradient_ms": med(lambda: qs.gradient(h2, p2), 10),
         "value_and_grad_ms": med(lambda: qs.value_and_grad(h2, p2), 10),
         "expectation": qs.expectation(h2, p2),
