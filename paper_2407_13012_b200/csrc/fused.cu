@@ -127,7 +127,9 @@ int pair_mode() {
 // Overrides QSB_SWEEP_R1 / QSB_SWEEP_R2 (plain sweeps, 3..6 / 3..4), QSB_SWEEP_R1M
 // (merged single-vector sweeps, 4..6) and QSB_SWEEP_R2M (merged bra/ket: 3 or 4) apply
 // to both window kinds.  6 = the R=5 shapes with two independent warp groups per CTA.
-int sweep_family(int nv, int mode, bool is_a) {
+// ftab: a sweep whose fp64 table tiles are TMA-staged, which only one-group kernels do
+// (sweep_impl.cuh TSTG): its single-vector sweeps stay on family 4.
+int sweep_family(int nv, int mode, bool is_a, bool ftab = false) {
   const bool merged = mode != SM_PLAIN;
   if (mode == SM_BRIDGE) return 4;
   if (merged && nv == 2) {
@@ -149,7 +151,7 @@ int sweep_family(int nv, int mode, bool is_a) {
   const char* e = getenv(merged ? "QSB_SWEEP_R1M" : (nv == 1 ? "QSB_SWEEP_R1" : "QSB_SWEEP_R2"));
   // (round 2, Z2-reduced chain: merged single-vector B sweeps on two R=5 warp groups,
   // 13.4 ms per C3 step vs 14.0 for R=4 and 16.5 for one R=5 group)
-  if (!e) return nv == 2 ? 4 : merged ? (is_a ? 4 : 6) : (is_a ? 6 : 4);
+  if (!e) return nv == 2 ? 4 : merged ? (is_a || ftab ? 4 : 6) : (is_a && !ftab ? 6 : 4);
   int r = atoi(e);
   if (merged) return (r == 5 || r == 6) ? r : 4;
   if (nv == 2 && r >= 5) r = 4;  // two vectors of 32 amplitudes do not fit in registers
@@ -164,10 +166,10 @@ int sweep_family(int nv, int mode, bool is_a) {
 // pair), qubits 12.. are stored bits 11.. (sh.lo / sh.hi / sh.glo: qubit numbering)
 int build_shape(const SweepShape& sh, int n, int nv, bool exact, SweepArgs& a, int gates_before_phase[kMaxPhases],
                 const int* pass2 = nullptr, int gates_before_phase2[kMaxPhases] = nullptr, int* gates2 = nullptr,
-                int mode = SM_PLAIN, int vshift = 0) {
+                int mode = SM_PLAIN, int vshift = 0, bool ftab = false) {
   int gl[kSweepT];
   for (int i = 0; i < kSweepT; ++i) gl[i] = sh.is_a ? i : (i < 3 ? i : sh.glo + i - 3);
-  const int fam = exact ? 4 : sweep_family(nv, mode, sh.is_a);
+  const int fam = exact ? 4 : sweep_family(nv, mode, sh.is_a, ftab);
   const int shape = pick_shape(exact, sh.is_a, fam);
   a.groups = fam == 6 ? 2 : 1;
   const int np = shape_np(shape);
@@ -472,8 +474,13 @@ struct Runner {
     SweepArgs a;
     memset(&a, 0, sizeof(a));
     int gbp[kMaxPhases], gbp2[kMaxPhases] = {0, 0, 0, 0}, gates2 = 0;
+    // merged / bridge sweeps over an fp64 table: TMA-stage each tile's table values for
+    // the mid ops, single-vector plain sweeps for their pre / post ops (QSB_NO_FTAB=1:
+    // read them from HBM per element)
+    const bool ftab = t && t->kind == 0 && t->values && !exact && !getenv("QSB_NO_FTAB") &&
+                      (mode != SM_PLAIN || (nv == 1 && (flags & (SF_PRE_PHASE | SF_POST_EXPECT))));
     const int gates = build_shape(sh, st(), nv, exact, a, gbp, mode != SM_PLAIN ? pass2 : nullptr, gbp2, &gates2, mode,
-                                  sym ? 1 : 0);
+                                  sym ? 1 : 0, ftab);
     if (gates < 0) return invalid("internal: bad sweep layout");
     a.mode = mode;
     {
@@ -493,9 +500,7 @@ struct Runner {
       if (nv == 2) QSB_TRY(encode_b_tile_map(&a.tm1, v1, st(), a.glo));
       if (a.cmode) QSB_TRY(encode_b_cidx_map(&a.tmc, t->cidx, t->kind == 1 ? 1 : 2, st(), a.glo));
     }
-    // merged / bridge sweeps over an fp64 table: TMA-stage each tile's table values for
-    // the mid ops (QSB_NO_FTAB=1: read them from HBM per element)
-    if (t && t->kind == 0 && t->values && !exact && mode != SM_PLAIN && !getenv("QSB_NO_FTAB")) {
+    if (ftab) {
       a.ftab = 1;
       if (!sh.is_a) QSB_TRY(encode_b_f64_map(&a.tmf, t->values, st(), a.glo));
     }

@@ -419,10 +419,10 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
   };
   auto wait_seq = [&](uint64_t s) { mbar_wait(seq_bar(s), (uint32_t)((s / (GR * kRing)) & 1)); };
   // fp64 table tile of a merged / bridge sweep (a.ftab): loaded into one slot at the tile
-  // start (every thread has passed the previous tile's mid ops by then -- there is a CTA
-  // barrier between), waited for just before the mid ops; the slot overlays the
-  // compact-index ring (fp64 tables have none)
-  constexpr bool TSTG = GR == 1 && MODE != SM_PLAIN && !KSIN && !EXACT;
+  // start (every thread has passed the previous tile's table reads by then -- there is a
+  // CTA barrier between), waited for just before the mid ops (plain single-vector sweeps:
+  // the pre / post ops); the slot overlays the compact-index ring (fp64 tables have none)
+  constexpr bool TSTG = GR == 1 && !EXACT && (MODE != SM_PLAIN ? !KSIN : NV == 1);
   const bool tstage = TSTG && a.ftab;
   const uint32_t tab_s = cring_s, tbar = bar_s + 8u * 8u;
   const double* tsm = (const double*)cring;
@@ -589,7 +589,8 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     // table-kind dispatch hoisted out of the unrolled loops (tv: value / phase views)
     auto with_table = [&](auto&& fn) {
       if constexpr (KSIN) {
-        fn(TvF64{a});
+        if (tstage) fn(TvF64S{a, tsm});
+        else fn(TvF64{a});
       } else {
         if (cmode == 2) fn(TvU8Rows{a, cs, slut, tb8, lrep, lq});
         else if (a.kind == 1) fn(TvU8{a, cs, slut, lrep, lq});
@@ -632,6 +633,7 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
           }
         }
       };
+      if (tstage) mbar_wait(tbar, tpar);  // the staged table tile serves the pre and post ops
       if (flags & (SF_PRE_PHASE | SF_BRA_FROM_KET | SF_PRE_DINNER)) with_table([&](auto tv) { pre_ops(tv); });
     }  // merged sweeps start and end mid-layer: no pre / post ops
 
