@@ -122,8 +122,9 @@ int pair_mode() {
 
 // register-bit family of the fast sweeps (measured per window kind, n=30 chain):
 // single-vector plain sweeps 6 on A windows (two R=5 warp groups) and 4 on B windows
-// (R=4, paired clusters); single-vector merged sweeps 4 on A, 5 on B; merged bra/ket
-// sweeps 4 on A, 3 on B (16 warps); other bra/ket sweeps 4.
+// (R=4, paired clusters); single-vector merged sweeps 4 on A, 6 on B (4 when an fp64
+// table is staged); merged bra/ket sweeps 4 on A, 3 on B (16 warps); other bra/ket
+// sweeps 4.
 // Overrides QSB_SWEEP_R1 / QSB_SWEEP_R2 (plain sweeps, 3..6 / 3..4), QSB_SWEEP_R1M
 // (merged single-vector sweeps, 4..6) and QSB_SWEEP_R2M (merged bra/ket: 3 or 4) apply
 // to both window kinds.  6 = the R=5 shapes with two independent warp groups per CTA.
