@@ -247,6 +247,9 @@ constexpr uint32_t mir_mask(uint32_t fm) { return fm == 0xffffffffu ? (0x1ffffff
 #ifndef QSB_TMA_STORE_B
 #define QSB_TMA_STORE_B 0  // 1: B tiles too (5-D tensor stores)
 #endif
+#ifndef QSB_LATE_KET
+#define QSB_LATE_KET 1  // staggered plain bra/ket sweeps without pre ops land the ket after the bra's first gates
+#endif
 #ifndef QSB_STAG_ARRIVE_ALL
 #define QSB_STAG_ARRIVE_ALL 1  // every thread arrives on the exchange mbarriers (0: one elected lane per warp after a __syncwarp -- same speed, but compute-sanitizer racecheck cannot follow it)
 #endif
@@ -304,6 +307,10 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
   constexpr bool STAG = NV == 2 && GR == 1 && !EXACT && FM != 0xffffffffu && (FM & kStagBit) != 0;
   constexpr bool STAG1 = STAG && MODE == SM_MERGED;  // staggered from the first stage
   constexpr bool STAGP = STAG && MODE == SM_PLAIN;
+  // staggered plain sweeps with no pre ops (the ket is not needed before stage 0): the
+  // ket lands after the bra's first gates, which hide part of its load latency (its TMA
+  // load is issued only when the previous tile releases both slots)
+  const bool late_ket = STAGP && QSB_LATE_KET && !(a.flags & (SF_PRE_PHASE | SF_BRA_FROM_KET | SF_PRE_DINNER));
   // single-vector A tiles leave through shared memory and a 1-D TMA store (no per-thread
   // global stores holding registers); the slot is reloaded once the store has read it.
   // (B tiles measured slower with 5-D tensor stores of 128-byte runs.)
@@ -504,11 +511,13 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
 #pragma unroll
         for (int j = 0; j < NR; ++j) v[1][j] = lds(xb_addr + nat(lb | ((uint32_t)j << P0.reg_l)) * 16u);
       }
-      if constexpr (!STAG1) {  // staggered: the ket lands in stage 0
-        wait_seq(2 * k + 1);
+      if constexpr (!STAG1) {  // staggered merged: the ket lands in stage 0
+        if (!late_ket) {
+          wait_seq(2 * k + 1);
 #pragma unroll
-        for (int j = 0; j < NR; ++j) v[0][j] = lds(xs_addr + nat(lb | ((uint32_t)j << P0.reg_l)) * 16u);
-        if constexpr (MIR) gsync();
+          for (int j = 0; j < NR; ++j) v[0][j] = lds(xs_addr + nat(lb | ((uint32_t)j << P0.reg_l)) * 16u);
+          if constexpr (MIR) gsync();
+        }
       }
     }
 
@@ -856,6 +865,14 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
           else gate_vec<FORM2, NR, R>(v[q], apply, a.ga2, a.gb2);
         };
         gates(QLc{});
+        if constexpr (s == 0 && MODE == SM_PLAIN) {
+          if (late_ket) {  // the lag lands (natural layout)
+            wait_seq(2 * k + 1);
+#pragma unroll
+            for (int j = 0; j < NR; ++j) v[0][j] = lds(xs_addr + nat(lb | ((uint32_t)j << M.reg_l)) * 16u);
+            if constexpr (MIR) gsync();
+          }
+        }
         if constexpr (s == 0 && MODE == SM_MERGED) {  // the lag lands (natural layout)
           wait_seq(2 * k + 1);
 #pragma unroll
