@@ -67,6 +67,7 @@ struct qsb_ctx {
   // calls, released when the context is destroyed or an allocation needs the memory
   std::vector<void*> ck;
   uint64_t ck_bytes = 0;
+  bool ck_busy = false;  // a walk using them is being enqueued (not released on OOM meanwhile)
   // live per-kernel profiling (qsb_prof_begin/end): CUDA events around each sweep
   bool prof = false;
   struct ProfRec {
@@ -121,6 +122,8 @@ int ensure_shot_scratch(qsb_ctx* ctx, uint64_t bytes);
 // free HBM above a margin (QSB_CKPT_MARGIN_GB, default 8; QSB_NO_CKPT=1: none)
 int ensure_checkpoints(qsb_ctx* ctx, uint64_t bytes, int want, std::vector<double2*>& out);
 void release_checkpoints(qsb_ctx* ctx);
+// the walk that ensure_checkpoints handed buffers to has enqueued its last use of them
+void checkpoints_done(qsb_ctx* ctx);
 // build (cos, sin) of (sign * gamma * v) for v = vmin + k, k < nvals, with host libm
 // (the same values Python's math.cos/sin and numba give) and upload to t->d_lut.
 int upload_phase_lut(qsb_table* t, double ang_scale, double2 extra_scale, bool exact);

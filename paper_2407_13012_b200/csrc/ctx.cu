@@ -99,37 +99,42 @@ int ensure_small(qsb_ctx* ctx, uint64_t bytes) {
 }
 
 // Forward checkpoints.  Contexts holding them are registered so an allocation that runs
-// out of memory can take the memory back (release_all_checkpoints).
+// out of memory (on any thread) can take the memory back (release_all_checkpoints).
+// g_ck_mu guards every context's ck / ck_bytes / ck_busy; a context whose walk is being
+// enqueued (ck_busy, from ensure_checkpoints to checkpoints_done) keeps its buffers.
 namespace {
 std::mutex g_ck_mu;
 std::unordered_set<qsb_ctx*> g_ck_ctxs;
-}  // namespace
 
-void release_checkpoints(qsb_ctx* ctx) {
+void release_locked(qsb_ctx* ctx) {  // g_ck_mu held
   if (ctx->ck.empty()) return;
   cudaSetDevice(ctx->device);
-  cudaStreamSynchronize(ctx->stream);
+  cudaStreamSynchronize(ctx->stream);  // kernels already enqueued may still read them
   for (void* p : ctx->ck) cudaFree(p);
   ctx->ck.clear();
   ctx->ck_bytes = 0;
-  std::lock_guard<std::mutex> g(g_ck_mu);
   g_ck_ctxs.erase(ctx);
+}
+}  // namespace
+
+void release_checkpoints(qsb_ctx* ctx) {
+  std::lock_guard<std::mutex> g(g_ck_mu);
+  release_locked(ctx);
 }
 
 void release_all_checkpoints() {
-  std::vector<qsb_ctx*> all;
-  {
-    std::lock_guard<std::mutex> g(g_ck_mu);
-    all.assign(g_ck_ctxs.begin(), g_ck_ctxs.end());
-  }
-  for (qsb_ctx* c : all) release_checkpoints(c);
+  std::lock_guard<std::mutex> g(g_ck_mu);
+  std::vector<qsb_ctx*> all(g_ck_ctxs.begin(), g_ck_ctxs.end());
+  for (qsb_ctx* c : all)
+    if (!c->ck_busy) release_locked(c);
 }
 
 int ensure_checkpoints(qsb_ctx* ctx, uint64_t bytes, int want, std::vector<double2*>& out) {
   out.clear();
   const char* off = getenv("QSB_NO_CKPT");
   if ((off && atoi(off)) || want <= 0) return QSB_OK;
-  if (ctx->ck_bytes != bytes) release_checkpoints(ctx);
+  std::lock_guard<std::mutex> g(g_ck_mu);
+  if (ctx->ck_bytes != bytes) release_locked(ctx);
   if ((int)ctx->ck.size() < want) {
     const char* m = getenv("QSB_CKPT_MARGIN_GB");
     const uint64_t margin = (uint64_t)(m ? atof(m) : 8.0) << 30;
@@ -145,13 +150,16 @@ int ensure_checkpoints(qsb_ctx* ctx, uint64_t bytes, int want, std::vector<doubl
       fr -= bytes;
     }
     ctx->ck_bytes = ctx->ck.empty() ? 0 : bytes;
-    if (!ctx->ck.empty()) {
-      std::lock_guard<std::mutex> g(g_ck_mu);
-      g_ck_ctxs.insert(ctx);
-    }
+    if (!ctx->ck.empty()) g_ck_ctxs.insert(ctx);
   }
   for (int i = 0; i < want && i < (int)ctx->ck.size(); ++i) out.push_back((double2*)ctx->ck[i]);
+  ctx->ck_busy = !out.empty();
   return QSB_OK;
+}
+
+void checkpoints_done(qsb_ctx* ctx) {
+  std::lock_guard<std::mutex> g(g_ck_mu);
+  ctx->ck_busy = false;
 }
 
 int prof_mark(qsb_ctx* ctx, cudaEvent_t* ev) {

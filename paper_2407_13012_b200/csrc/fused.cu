@@ -742,6 +742,13 @@ int run_chain(Runner& R, double2* ket, double2* bra, int p, const double* gammas
   // phase at the start of the next sweep instead)
   const bool ck_ok = R.want_ck && fwd && bwd && merge;
   if (ck_ok) QSB_TRY(ensure_checkpoints(R.ctx, 16ull << R.st(), F, R.ck));
+  struct CkDone {  // every return path: the buffers may be released again once enqueued
+    qsb_ctx* c;
+    bool on;
+    ~CkDone() {
+      if (on) checkpoints_done(c);
+    }
+  } ck_done{R.ctx, ck_ok};
   const int K = ck_ok ? std::min<int>((int)R.ck.size(), F) : 0;
   if (K > 0) R.defer = false;  // checkpoints hold true values: no scale carried along the chain
   int fj = 0, bj = 0;  // forward / backward jobs launched so far
