@@ -567,6 +567,21 @@ def small_configs() -> dict:
     return out
 
 
+# bare-I/O ceilings of the bra/ket access patterns on this GPU (tools/probe_braket_io.cu,
+# profiles/r2_probe_braket_io.txt: read bra + read ket + write bra through the library's TMA
+# ring, no arithmetic), n=29; the middle (plain) B window sits at stored bit 11
+PATTERN_CEILING_GBS = {"braket_B": 5791.9, "braket_A": 6670.2}
+
+
+def pattern_ceiling(kind: str, achieved: float) -> dict:
+    c = PATTERN_CEILING_GBS.get(kind)
+    if c is None:
+        return {}
+    return {"pattern_ceiling": {"value": c, "unit": "GB/s", "frac": achieved / c,
+                                "source": "profiles/r2_probe_braket_io.txt: bare I/O of the same tile pattern "
+                                          "(48 B/amp, TMA ring, no arithmetic), measured on a B200"}}
+
+
 def run_b200(args, rank: int, world: int, dist) -> None:
     import numpy as np
 
@@ -695,6 +710,7 @@ def run_b200(args, rank: int, world: int, dist) -> None:
             "traffic": traffic,
             "launches_per_step": n_l / args.steps,
             "alg_bytes_per_launch": b / n_l,
+            **pattern_ceiling(dom, achieved),
         },
         "kernels": {
             k: {"launches_per_step": v[0] / args.steps, "ms_per_step": v[1] / args.steps,
