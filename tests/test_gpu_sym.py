@@ -99,3 +99,31 @@ def test_forward_checkpoints(n, p, sym, monkeypatch):
     plus = np.full(1 << n, 1.0 / np.sqrt(float(1 << n)))
     assert np.max(np.abs(np.asarray(h.state.data) - plus)) <= 1e-12
     h.close()
+
+
+def test_checkpoints_given_back_when_memory_runs_out():
+    """checkpoints cached with a context are spare HBM: an allocation that finds the
+    device full takes them back (ctx.cu plain_alloc -> release_all_checkpoints) and
+    succeeds, and the next gradient rebuilds them with the same result"""
+    import ctypes as C
+
+    from paper_2407_13012_b200._lib import call
+
+    n, p = 27, 3
+    poly = random_instance(1300 + n, n)
+    params = random_params(5, p)
+    h = qs.create_handle(poly, backend_name="b200")
+    v, g = qs.value_and_grad(h, params)  # leaves >= 3 GiB of checkpoints on h's context
+    dev = h.ctx.device
+    _, free0, _ = dev.info()
+    ptr = C.c_void_p()
+    call("qsb_alloc", dev.handle, free0 + (512 << 20), C.byref(ptr))  # more than is free
+    try:
+        assert ptr.value
+    finally:
+        call("qsb_free", dev.handle, ptr)
+    v2, g2 = qs.value_and_grad(h, params)
+    assert v2 == v
+    assert np.array_equal(np.asarray(g2.d_gammas), np.asarray(g.d_gammas))
+    assert np.array_equal(np.asarray(g2.d_betas), np.asarray(g.d_betas))
+    h.close()
