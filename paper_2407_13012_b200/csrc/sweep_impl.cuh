@@ -940,7 +940,9 @@ __global__ void __launch_bounds__(GR * (32 << shape_w(SH)), 1) k_sweep(const __g
     // NV=1: order this tile's generic-proxy smem writes (exchanges) before the TMA that
     // will refill the slot.  Fenced here, ahead of the global stores: the fence's
     // MEMBAR then does not wait for this tile's 64 KB of stores to drain.
-    const bool tma_out = TMAST && a.sw_g == 0 && !(flags & SF_NO_STORE);
+    // (B tiles: the 5-D store map is the input's, so out-of-place sweeps -- forward
+    // checkpoints -- store from registers)
+    const bool tma_out = TMAST && a.sw_g == 0 && !(flags & SF_NO_STORE) && (IS_A || !a.o0);
     if (tma_out) {
       // natural layout (the final map puts quarter-warp lanes on local bits 0..2:
       // conflict-free, and each 8-amplitude chunk is the warp's own -- a warp barrier
