@@ -8,7 +8,9 @@ for rep in 1 2; do
 import json, sys
 d = json.loads(sys.argv[2])
 k = d["kernels"]
-print(f"[{sys.argv[1] or 'default'}] {d['ms_per_step']:.1f} ms  " + " ".join(f"{n}={v['ms_per_step']:.1f}" for n, v in sorted(k.items())))
+# the expectation is printed so a variant that computes something else shows up at once
+print(f"[{sys.argv[1] or 'default'}] {d['ms_per_step']:.1f} ms  E={d['expectation']:.12f}  " +
+      " ".join(f"{n}={v['ms_per_step']:.1f}" for n, v in sorted(k.items())))
 PY
   done
 done
