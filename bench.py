@@ -8,10 +8,12 @@ simulation from |+>, <C>, and the gradient over all 2p angles (bra/ket adjoint
 walk).  Inputs are resident in HBM (the cost table, built once per handle);
 the 16 GiB statevector exceeds the 126 MB L2 by >100x, so no L2 flush is needed.
 For N > 1 (torchrun, one process per GPU) the statevector is sharded over the N
-GPUs (paper_2407_13012_b200/dist.py: top log2 N qubits global, NCCL all-to-all
-index-bit swaps); weak scaling keeps 2^30 amplitudes per GPU (n = 30 + log2 N)
-and value counts n=30-equivalent evaluations (steps * 2^(n-30) / max-over-ranks
-device time).  `--replicas` runs N independent n=30 replicas instead.
+GPUs (paper_2407_13012_b200/dist.py: top log2 N qubits global, qubit swaps fused into
+the sweeps' stores over NVLink P2P, or NCCL all-to-all); weak scaling keeps 2^31
+amplitudes per GPU (BASELINE config 5's ladder, n = 31 + log2 N: n=34 on 8 GPUs) plus
+config 4's n=32 p=8 lines at N = 2 and 4 (see run_sharded), and value counts
+n=30-equivalent evaluations (steps * 2^(n-30) / max-over-ranks device time).
+`--replicas` runs N independent n=30 replicas instead.
 
 `--impl reference` times the reference's CPU path on the host cores instead:
 measured end-to-end E+grad evaluations (the reference's expectation + gradient

@@ -695,10 +695,22 @@ std::vector<Visit> chain_visits(int n, const std::vector<SweepShape>& wins, int 
 
 // Runs forward layers 0..p-1 (fwd) and/or the adjoint walk p-1..0 (bwd) as one chain
 // of sweeps.  Contributions to <C> / d_gamma / d_beta are recorded in `contribs`.
+// Window order of the chain's layers.  Merged sweeps (FP64 / shared-memory bound) land
+// on the two END windows of the order, plain (HBM-bound) visits on the middle ones.
+// QSB_WIN_ORDER=mid puts the A window second (B1, A, B2, ..): merged sweeps then run on
+// 9-qubit B windows (less FP64 per amplitude than A's 12) and the plain visits on the
+// contiguous A tiles (the fastest HBM pattern).  Default: A first (A, B1, B2, ..).
+std::vector<SweepShape> chain_windows(const std::vector<SweepShape>& shapes) {
+  std::vector<SweepShape> w = shapes;
+  const char* e = getenv("QSB_WIN_ORDER");
+  if (e && strcmp(e, "mid") == 0 && w.size() >= 3 && w[0].is_a) std::swap(w[0], w[1]);
+  return w;
+}
+
 int run_chain(Runner& R, double2* ket, double2* bra, int p, const double* gammas, const double* betas, bool fwd,
               bool from_plus, bool want_value, bool bwd, std::vector<Contrib>& contribs) {
   const int n = R.n;
-  const std::vector<SweepShape>& wins = R.shapes;
+  const std::vector<SweepShape> wins = chain_windows(R.shapes);
   const std::vector<Visit> vis = chain_visits(n, wins, p, fwd, bwd);
   const int M = (int)vis.size();
   const bool merge = merge_enabled() && wins.size() >= 2;
