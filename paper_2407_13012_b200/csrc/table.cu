@@ -9,7 +9,12 @@
 // non-matching term is exactly what the reference does, so the sum is bit-exact
 // for any weights.
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
 
 #include "common.cuh"
 
@@ -74,6 +79,108 @@ __global__ void __launch_bounds__(kPreThreads) k_precompute(const double* __rest
   }
 }
 
+// ---------------------------------------------------------------- dyadic-weight path
+// When every weight is a multiple of 2^-s and sum |w| * 2^s < 2^52, every partial sum
+// of the reference's term-ordered loop is a multiple of 2^-s below 2^(52-s) in
+// magnitude -- exactly representable -- so each addition is exact and T[x] is the
+// exact sum of the matching weights, whatever the order.  (Integer weights -- every
+// MaxCut / weighted MaxCut -- are the case s = 0.)  That sum is then computed in int64
+// tile by tile: a tile is 4096 consecutive x sharing their high bits xh; a term with
+// mask m contributes to the tile iff (m & ~0xFFF) is inside xh, and then to every x
+// whose low 12 bits contain m & 0xFFF.  So W[l] = sum of those terms' weights with
+// m & 0xFFF == l, and T[xh | x] = sum over l subset of x of W[l]: a subset-sum (zeta)
+// transform over 12 bits -- 12 adds per x instead of one mask test per term.
+// The bit-exact equality with the term-ordered double sum is what the tests check.
+constexpr int kZT = 12;                 // tile bits
+constexpr int kZThreads = 256;          // 16 entries per thread
+constexpr uint32_t kZN = 1u << kZT;
+
+// shared-memory word of entry x: bits 4..7 XORed into bits 0..3, so each of the three
+// register maps below reads/writes 16 consecutive words per half-warp (conflict-free)
+__device__ __forceinline__ uint32_t zswz(uint32_t x) { return x ^ ((x >> 4) & 15u); }
+
+// zeta over the 4 register bits of v (v[r] += v[r without bit b] for every set bit b)
+__device__ __forceinline__ void zeta_regs(long long (&v)[16]) {
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      if (r & (1 << b)) v[r] += v[r ^ (1 << b)];
+}
+
+__global__ void __launch_bounds__(kZThreads) k_precompute_zeta(const long long* __restrict__ w,
+                                                               const uint64_t* __restrict__ m, uint64_t num_terms,
+                                                               double* __restrict__ out, uint64_t ntiles, double scale,
+                                                               IndexMap map) {
+  __shared__ long long S[kZN];
+  const uint32_t tid = threadIdx.x, lane = tid & 31u;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t i0 = tile << kZT;
+    const uint64_t xh = map(i0);  // the tile's high bits (the map is the identity on bits < 12)
+#pragma unroll
+    for (int r = 0; r < 16; ++r) S[tid + 256u * r] = 0;
+    __syncthreads();
+    // scatter the tile's terms; those with no low bits (the common case for high
+    // qubits) are summed in registers and added once per warp
+    long long c0 = 0;
+    for (uint64_t k = tid; k < num_terms; k += kZThreads) {
+      const uint64_t mk = __ldg(&m[k]);
+      if ((mk & ~(uint64_t)(kZN - 1u)) & ~xh) continue;  // a high bit the tile lacks
+      const uint32_t lo = (uint32_t)(mk & (kZN - 1u));
+      const long long wk = __ldg(&w[k]);
+      if (lo == 0) c0 += wk;
+      else atomicAdd((unsigned long long*)&S[zswz(lo)], (unsigned long long)wk);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+    if (lane == 0 && c0) atomicAdd((unsigned long long*)&S[0], (unsigned long long)c0);
+    __syncthreads();
+    long long v[16];
+    // map 3: registers = bits 0..3, lanes = bits 4..8, warps = bits 9..11
+    {
+      const uint32_t base = tid << 4;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) v[r] = S[zswz(base | r)];
+      zeta_regs(v);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) S[zswz(base | r)] = v[r];
+    }
+    __syncthreads();
+    // map 2: registers = bits 4..7, lanes = bits 0..3 and 8, warps = bits 9..11
+    {
+      const uint32_t base = (tid & 15u) | ((tid >> 4) << 8);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) v[r] = S[zswz(base | (r << 4))];
+      zeta_regs(v);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) S[zswz(base | (r << 4))] = v[r];
+    }
+    __syncthreads();
+    // map 1: registers = bits 8..11, threads = bits 0..7 -> coalesced stores
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = S[zswz(tid | (r << 8))];
+    zeta_regs(v);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) __stcs(out + i0 + tid + 256u * r, (double)v[r] * scale);
+    __syncthreads();  // S is zeroed for the next tile
+  }
+}
+
+// the dyadic scale s of the weights (see above), or -1 when the path does not apply
+static int dyadic_shift(const double* w, uint64_t num_terms) {
+  for (int sh = 0; sh <= 24; ++sh) {
+    double tot = 0.0;
+    bool ok = true;
+    for (uint64_t k = 0; k < num_terms && ok; ++k) {
+      const double x = ldexp(w[k], sh);
+      ok = std::isfinite(x) && x == rint(x);
+      tot += fabs(x);
+    }
+    if (ok) return tot < 4503599627370496.0 ? sh : -1;  // 2^52 (tot itself rounds up at worst)
+  }
+  return -1;
+}
+
 // compact index: idx = T - vmin when T is an integer; flags non-integral values
 template <typename IDX>
 __global__ void k_compact(const double* __restrict__ t, uint64_t len, double vmin, IDX* __restrict__ idx,
@@ -100,6 +207,24 @@ static int precompute_into(qsb_ctx* ctx, const double* weights, const int64_t* m
   QSB_TRY(ensure_small(ctx, tbytes + 64));
   double* dw = (double*)ctx->d_small;
   uint64_t* dm = (uint64_t*)(dw + num_terms);
+  // dyadic weights over whole 4096-x tiles: the exact int64 subset-sum path
+  const char* nz = getenv("QSB_NO_ZETA");
+  const int sh = (len >= kZN && (len & (kZN - 1)) == 0 && map.b >= (uint32_t)kZT && !(nz && atoi(nz))) ? dyadic_shift(weights, num_terms) : -1;
+  if (sh >= 0) {
+    std::vector<long long> iw(num_terms);
+    for (uint64_t k = 0; k < num_terms; ++k) iw[k] = (long long)ldexp(weights[k], sh);
+    if (num_terms) {
+      QSB_CUDA(cudaMemcpyAsync(dw, iw.data(), num_terms * sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
+      QSB_CUDA(cudaMemcpyAsync(dm, masks, num_terms * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    const uint64_t ntiles = len >> kZT;
+    const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * 3);  // 80 registers: 3 CTAs per SM
+    k_precompute_zeta<<<(unsigned)grid, kZThreads, 0, ctx->stream>>>((const long long*)dw, dm, num_terms, out, ntiles,
+                                                                     ldexp(1.0, -sh), map);
+    QSB_CHECK_LAUNCH(ctx, "precompute (dyadic)");
+    QSB_CUDA(cudaStreamSynchronize(ctx->stream));  // host term arrays / d_small reuse
+    return QSB_OK;
+  }
   if (num_terms) {
     // d_small may still be read by queued kernels -> synchronous, stream-ordered copies
     QSB_CUDA(cudaMemcpyAsync(dw, weights, num_terms * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));

@@ -6,6 +6,7 @@ sincos, <= 1e-15 as the reference's own cross-set tolerance)."""
 import numpy as np
 import pytest
 
+import paper_2407_13012_b200 as qs
 from paper_2407_13012_b200 import backend as be
 from paper_2407_13012_b200.errors import ContractViolation
 from paper_2407_13012_b200.kernels import b200
@@ -122,6 +123,36 @@ def test_precompute_random_polynomials_bitwise(ctx, n, terms):
     want = oracle.precompute_table(w, m, n)
     assert np.array_equal(np.asarray(out), want)
     assert (lo, hi) == (want.min(), want.max())
+
+
+@pytest.mark.parametrize("n,terms,shift,deg", [(12, 40, 0, 2), (13, 200, 0, 2), (16, 500, 3, 4), (20, 1500, 1, 2),
+                                               (22, 90, 0, 6), (14, 0, 0, 2)])
+def test_precompute_dyadic_bitwise(ctx, n, terms, shift, deg):
+    """Dyadic weights (multiples of 2^-shift, negatives, any degree): the exact int64
+    subset-sum path (table.cu k_precompute_zeta) equals the reference's term-ordered
+    double sum bit for bit, and so does the per-term kernel (QSB_NO_ZETA=1)."""
+    r = np.random.default_rng(100 + n)
+    w = r.integers(-9, 10, terms).astype(np.float64) / (1 << shift)
+    m = np.zeros(terms, dtype=np.int64)
+    for k in range(terms):
+        bits = r.choice(n, size=int(r.integers(0, deg + 1)), replace=False)
+        m[k] = int(sum(1 << int(b) for b in bits))
+    want = oracle.precompute_table(w, m, n)
+    out = b200.empty(ctx.device, 1 << n, np.float64)
+    lo, hi = b200.build_cost_table(n, w, m, out)
+    assert np.array_equal(np.asarray(out), want)
+    assert not np.signbit(np.asarray(out)[np.asarray(out) == 0]).any()  # +0.0 like the reference
+    assert (lo, hi) == (want.min(), want.max())
+
+
+def test_precompute_dyadic_matches_per_term_kernel(ctx, monkeypatch):
+    poly = qs.maxcut_polynomial(qs.erdos_renyi(21, 0.5, seed=3))
+    a = b200.empty(ctx.device, 1 << 21, np.float64)
+    b200.build_cost_table(21, poly.weights, poly.masks, a)
+    monkeypatch.setenv("QSB_NO_ZETA", "1")
+    b = b200.empty(ctx.device, 1 << 21, np.float64)
+    b200.build_cost_table(21, poly.weights, poly.masks, b)
+    assert np.array_equal(np.asarray(a), np.asarray(b))
 
 
 def test_pairwise_level(ctx):
