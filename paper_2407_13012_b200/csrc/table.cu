@@ -211,15 +211,32 @@ static int precompute_into(qsb_ctx* ctx, const double* weights, const int64_t* m
   const char* nz = getenv("QSB_NO_ZETA");
   const int sh = (len >= kZN && (len & (kZN - 1)) == 0 && map.b >= (uint32_t)kZT && !(nz && atoi(nz))) ? dyadic_shift(weights, num_terms) : -1;
   if (sh >= 0) {
-    std::vector<long long> iw(num_terms);
-    for (uint64_t k = 0; k < num_terms; ++k) iw[k] = (long long)ldexp(weights[k], sh);
-    if (num_terms) {
-      QSB_CUDA(cudaMemcpyAsync(dw, iw.data(), num_terms * sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
-      QSB_CUDA(cudaMemcpyAsync(dm, masks, num_terms * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+    // exact sums: terms with equal masks merge into one (MaxCut's x_i terms repeat once
+    // per edge), zero sums drop out; ascending masks put the terms of one tile-high
+    // part on consecutive lanes with distinct low parts (few same-address atomics)
+    std::vector<std::pair<uint64_t, long long>> tm(num_terms);
+    for (uint64_t k = 0; k < num_terms; ++k) tm[k] = {(uint64_t)masks[k], (long long)ldexp(weights[k], sh)};
+    std::sort(tm.begin(), tm.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+    std::vector<long long> iw;
+    std::vector<uint64_t> im;
+    for (uint64_t k = 0; k < num_terms;) {
+      uint64_t e = k;
+      long long sum = 0;
+      for (; e < num_terms && tm[e].first == tm[k].first; ++e) sum += tm[e].second;
+      if (sum) {
+        iw.push_back(sum);
+        im.push_back(tm[k].first);
+      }
+      k = e;
+    }
+    const uint64_t nt = iw.size();
+    if (nt) {
+      QSB_CUDA(cudaMemcpyAsync(dw, iw.data(), nt * sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
+      QSB_CUDA(cudaMemcpyAsync(dm, im.data(), nt * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
     }
     const uint64_t ntiles = len >> kZT;
     const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * 3);  // 80 registers: 3 CTAs per SM
-    k_precompute_zeta<<<(unsigned)grid, kZThreads, 0, ctx->stream>>>((const long long*)dw, dm, num_terms, out, ntiles,
+    k_precompute_zeta<<<(unsigned)grid, kZThreads, 0, ctx->stream>>>((const long long*)dw, dm, nt, out, ntiles,
                                                                      ldexp(1.0, -sh), map);
     QSB_CHECK_LAUNCH(ctx, "precompute (dyadic)");
     QSB_CUDA(cudaStreamSynchronize(ctx->stream));  // host term arrays / d_small reuse

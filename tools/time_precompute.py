@@ -20,6 +20,7 @@ from paper_2407_13012_b200.kernels import b200
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--max-n", type=int, default=32)
+ap.add_argument("--only", default=None, help="comma list of problem names")
 args = ap.parse_args()
 
 ctx = be.create_context("b200")
@@ -36,11 +37,11 @@ def build(poly, out):
 cases = [("reg3", n, lambda n: qs.maxcut_polynomial(qs.random_regular(n, 3, seed=1))) for n in (24, 28, 30)]
 cases += [("er0.5", n, lambda n: qs.maxcut_polynomial(qs.erdos_renyi(n, 0.5, seed=1))) for n in (24, 29)]
 cases += [("wK", n, lambda n: bench.weighted_maxcut(n, 1)) for n in (28, 32)]
-cases += [("qubo(float)", 28, lambda n: bench.qubo_polynomial(n, 1))]
+cases += [("qubo(float)", n, lambda n: bench.qubo_polynomial(n, 1)) for n in (28, 32)]
 os.environ.setdefault("QAOA_MAX_QUBITS", "34")
 os.environ.setdefault("QAOA_MEM_CEILING_BYTES", str(16 << 32))
 for name, n, mk in cases:
-    if n > args.max_n:
+    if n > args.max_n or (args.only and name not in args.only.split(",")):
         continue
     poly = mk(n)
     out = b200.empty(ctx.device, 1 << n, np.float64)
