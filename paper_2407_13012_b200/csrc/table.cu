@@ -13,7 +13,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
+#include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
@@ -111,9 +113,10 @@ __device__ __forceinline__ void zeta_regs(long long (&v)[16]) {
 __global__ void __launch_bounds__(kZThreads) k_precompute_zeta(const long long* __restrict__ w,
                                                                const uint64_t* __restrict__ m, uint64_t num_terms,
                                                                double* __restrict__ out, uint64_t ntiles, double scale,
-                                                               IndexMap map) {
+                                                               IndexMap map, long long* __restrict__ minmax) {
   __shared__ long long S[kZN];
   const uint32_t tid = threadIdx.x, lane = tid & 31u;
+  long long vlo = LLONG_MAX, vhi = LLONG_MIN;  // the table's min / max (int64, fused)
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint64_t i0 = tile << kZT;
     const uint64_t xh = map(i0);  // the tile's high bits (the map is the identity on bits < 12)
@@ -161,9 +164,59 @@ __global__ void __launch_bounds__(kZThreads) k_precompute_zeta(const long long* 
     for (int r = 0; r < 16; ++r) v[r] = S[zswz(tid | (r << 8))];
     zeta_regs(v);
 #pragma unroll
-    for (int r = 0; r < 16; ++r) __stcs(out + i0 + tid + 256u * r, (double)v[r] * scale);
+    for (int r = 0; r < 16; ++r) {
+      __stcs(out + i0 + tid + 256u * r, (double)v[r] * scale);
+      vlo = min(vlo, v[r]);
+      vhi = max(vhi, v[r]);
+    }
     __syncthreads();  // S is zeroed for the next tile
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    vlo = min(vlo, __shfl_xor_sync(0xffffffffu, vlo, o));
+    vhi = max(vhi, __shfl_xor_sync(0xffffffffu, vhi, o));
+  }
+  if (lane == 0) {
+    atomicMin(&minmax[0], vlo);
+    atomicMax(&minmax[1], vhi);
+  }
+}
+
+__global__ void k_minmax_init(long long* mm) {
+  mm[0] = LLONG_MAX;
+  mm[1] = LLONG_MIN;
+}
+
+// Exact flip symmetry of a table given by merged integer terms W_m (T(x) = sum of W_m over
+// m subset of x): T(~x) = sum_m W_m prod_{i in m} (1 - x_i) has the subset-basis
+// coefficients D_s = (-1)^|s| sum_{m superset of s} W_m, and the basis is unique, so
+// T(x) == T(~x) for every x iff D == W.  The tables of this path are exact integer sums,
+// so this equals the device check values[x] == values[len-1-x] bit for bit.
+// Returns 1 / 0, or -1 when the subset enumeration would be too large.
+static int dyadic_symmetric(const std::vector<uint64_t>& im, const std::vector<long long>& iw) {
+  uint64_t work = 0;
+  for (uint64_t m : im) {
+    const int d = __builtin_popcountll(m);
+    if (d > 20) return -1;
+    work += 1ull << d;
+    if (work > (1ull << 22)) return -1;
+  }
+  std::unordered_map<uint64_t, long long> D;
+  D.reserve(work * 2);
+  for (size_t k = 0; k < im.size(); ++k) {
+    const uint64_t m = im[k];
+    for (uint64_t sub = m;; sub = (sub - 1) & m) {  // every subset of m
+      D[sub] += (__builtin_popcountll(sub) & 1) ? -iw[k] : iw[k];
+      if (!sub) break;
+    }
+  }
+  std::unordered_map<uint64_t, long long> W;
+  for (size_t k = 0; k < im.size(); ++k) W[im[k]] = iw[k];  // masks are unique here
+  for (const auto& [sub, c] : D)
+    if (c != 0 && (W.count(sub) ? W[sub] : 0) != c) return 0;
+  for (const auto& [m, c] : W)
+    if ((D.count(m) ? D[m] : 0) != c) return 0;
+  return 1;
 }
 
 // the dyadic scale s of the weights (see above), or -1 when the path does not apply
@@ -201,8 +254,17 @@ namespace qsb {
 
 int minmax(qsb_ctx* ctx, const double* v, uint64_t len, double* mn, double* mx);  // ops.cu
 
+// what a precompute already knows about its table (the dyadic path: min / max from the
+// kernel, flip symmetry from the terms) -- finish_table skips those passes
+struct TableStats {
+  bool minmax = false;
+  double vmin = 0, vmax = 0;
+  int sym = -1;  // -1 unknown
+};
+
 static int precompute_into(qsb_ctx* ctx, const double* weights, const int64_t* masks, uint64_t num_terms,
-                           double* out, uint64_t len, IndexMap map = IndexMap{63, 63, 0, 0}) {
+                           double* out, uint64_t len, IndexMap map = IndexMap{63, 63, 0, 0},
+                           TableStats* stats = nullptr) {
   const uint64_t tbytes = num_terms * (sizeof(double) + sizeof(uint64_t));
   QSB_TRY(ensure_small(ctx, tbytes + 64));
   double* dw = (double*)ctx->d_small;
@@ -236,10 +298,24 @@ static int precompute_into(qsb_ctx* ctx, const double* weights, const int64_t* m
     }
     const uint64_t ntiles = len >> kZT;
     const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * 3);  // 80 registers: 3 CTAs per SM
+    QSB_TRY(ensure_scratch(ctx, 64));
+    long long* dmm = (long long*)ctx->d_scratch;
+    k_minmax_init<<<1, 1, 0, ctx->stream>>>(dmm);
     k_precompute_zeta<<<(unsigned)grid, kZThreads, 0, ctx->stream>>>((const long long*)dw, dm, nt, out, ntiles,
-                                                                     ldexp(1.0, -sh), map);
+                                                                     ldexp(1.0, -sh), map, dmm);
     QSB_CHECK_LAUNCH(ctx, "precompute (dyadic)");
+    long long hmm[2];
+    QSB_CUDA(cudaMemcpyAsync(hmm, dmm, sizeof(hmm), cudaMemcpyDeviceToHost, ctx->stream));
+    // (the host symmetry test overlaps the kernel)
+    const bool identity = map.b >= 63;
+    const int sym = identity ? dyadic_symmetric(im, iw) : -1;
     QSB_CUDA(cudaStreamSynchronize(ctx->stream));  // host term arrays / d_small reuse
+    if (stats) {
+      stats->minmax = true;
+      stats->vmin = (double)hmm[0] * ldexp(1.0, -sh);
+      stats->vmax = (double)hmm[1] * ldexp(1.0, -sh);
+      stats->sym = sym;
+    }
     return QSB_OK;
   }
   if (num_terms) {
@@ -264,10 +340,19 @@ __global__ void k_symcheck(const double* __restrict__ v, uint64_t len, int* bad)
   if (!__syncthreads_and(ok) && threadIdx.x == 0) atomicOr(bad, 1);
 }
 
-static int finish_table(qsb_ctx* ctx, qsb_table* t) {
-  QSB_TRY(minmax(ctx, t->values, t->len, &t->vmin, &t->vmax));
+static int finish_table(qsb_ctx* ctx, qsb_table* t, const TableStats* known = nullptr) {
+  const char* nk = getenv("QSB_NO_TABLE_STATS");  // A/B + tests: recompute on the device
+  if (nk && atoi(nk)) known = nullptr;
+  if (known && known->minmax) {
+    t->vmin = known->vmin;
+    t->vmax = known->vmax;
+  } else {
+    QSB_TRY(minmax(ctx, t->values, t->len, &t->vmin, &t->vmax));
+  }
   t->sym = 0;
-  if (t->len >= 2) {
+  if (known && known->sym >= 0) {
+    t->sym = t->len >= 2 ? known->sym : 0;
+  } else if (t->len >= 2) {
     QSB_TRY(ensure_scratch(ctx, 64));
     int* bad = (int*)ctx->d_scratch;
     QSB_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
@@ -344,6 +429,28 @@ int upload_phase_lut(qsb_table* t, double ang_scale, double2 extra, bool exact) 
 
 int launch_phase_lut(qsb_ctx* ctx, qsb_table* t, double2* amps);  // ops.cu
 
+static int wrap_table(qsb_ctx* ctx, int n, double* values, double* min_out, double* max_out, qsb_table** out,
+                      const TableStats* known) {
+  if (ctx) QSB_CUDA(cudaSetDevice(ctx->device));  // launches go to the context's GPU
+  if (!ctx || !values || !out) return invalid("qsb_table_wrap: null argument");
+  if (n < 1 || n > 62) return invalid("qsb_table_wrap: n=%d out of range", n);
+  qsb_table* t = new qsb_table();
+  t->ctx = ctx;
+  t->n = n;
+  t->len = 1ull << n;
+  t->values = values;
+  int rc = finish_table(ctx, t, known);
+  if (rc != QSB_OK) {
+    qsb_table_destroy(t);
+    return rc;
+  }
+  if (min_out) *min_out = t->vmin;
+  if (max_out) *max_out = t->vmax;
+  *out = t;
+  return QSB_OK;
+}
+
+
 }  // namespace qsb
 
 extern "C" {
@@ -363,8 +470,9 @@ int qsb_table_create(qsb_ctx* ctx, int n, const double* weights, const int64_t* 
   const uint64_t len = 1ull << n;
   for (uint64_t k = 0; k < num_terms; ++k)
     if (masks[k] < 0 || (uint64_t)masks[k] >= len) return invalid("term mask %lld out of range for n=%d", (long long)masks[k], n);
-  QSB_TRY(precompute_into(ctx, weights, masks, num_terms, values, len));
-  return qsb_table_wrap(ctx, n, values, min_out, max_out, out);
+  TableStats st;
+  QSB_TRY(precompute_into(ctx, weights, masks, num_terms, values, len, IndexMap{63, 63, 0, 0}, &st));
+  return wrap_table(ctx, n, values, min_out, max_out, out, &st);
 }
 
 // Shard of a 2^n_global table: local index i of `rank` under the layout map
@@ -381,28 +489,13 @@ int qsb_table_create_mapped(qsb_ctx* ctx, int n_global, int n_local, const doubl
       return invalid("term mask %lld out of range for n=%d", (long long)masks[k], n_global);
   if (b < 2 || b > n_local) return invalid("index map needs 2 <= b <= n_local (b=%d)", b);
   IndexMap map{(uint32_t)b, (uint32_t)s1, (uint32_t)s2, rank};
-  QSB_TRY(precompute_into(ctx, weights, masks, num_terms, values, 1ull << n_local, map));
-  return qsb_table_wrap(ctx, n_local, values, min_out, max_out, out);
+  TableStats st;
+  QSB_TRY(precompute_into(ctx, weights, masks, num_terms, values, 1ull << n_local, map, &st));
+  return wrap_table(ctx, n_local, values, min_out, max_out, out, &st);
 }
 
 int qsb_table_wrap(qsb_ctx* ctx, int n, double* values, double* min_out, double* max_out, qsb_table** out) {
-  if (ctx) QSB_CUDA(cudaSetDevice(ctx->device));  // launches go to the context's GPU
-  if (!ctx || !values || !out) return invalid("qsb_table_wrap: null argument");
-  if (n < 1 || n > 62) return invalid("qsb_table_wrap: n=%d out of range", n);
-  qsb_table* t = new qsb_table();
-  t->ctx = ctx;
-  t->n = n;
-  t->len = 1ull << n;
-  t->values = values;
-  int rc = finish_table(ctx, t);
-  if (rc != QSB_OK) {
-    qsb_table_destroy(t);
-    return rc;
-  }
-  if (min_out) *min_out = t->vmin;
-  if (max_out) *max_out = t->vmax;
-  *out = t;
-  return QSB_OK;
+  return wrap_table(ctx, n, values, min_out, max_out, out, nullptr);
 }
 
 // Does not touch t->ctx (it may already be destroyed); cudaFree synchronises.

@@ -145,6 +145,40 @@ def test_precompute_dyadic_bitwise(ctx, n, terms, shift, deg):
     assert (lo, hi) == (want.min(), want.max())
 
 
+@pytest.mark.parametrize("kind", ["maxcut", "weighted_maxcut", "spin_even", "spin_odd", "random"])
+def test_dyadic_table_stats_match_device_passes(ctx, kind, monkeypatch):
+    """The dyadic path's fused min/max and its host (term-algebra) flip-symmetry test
+    give exactly what the device passes find on the table (QSB_NO_TABLE_STATS=1)."""
+    n = 18
+    r = np.random.default_rng(7)
+    if kind == "maxcut":
+        poly = qs.maxcut_polynomial(qs.erdos_renyi(n, 0.3, seed=5))
+    elif kind == "weighted_maxcut":
+        edges = [(u, v, float(r.integers(1, 9))) for u in range(n) for v in range(u + 1, n) if r.random() < 0.4]
+        poly = qs.maxcut_polynomial(qs.Graph(n, edges))
+    elif kind.startswith("spin"):  # spin monomials of even (symmetric) or mixed degree, expanded to boolean
+        deg = [2, 4] if kind == "spin_even" else [1, 2, 3]
+        terms = []
+        for _ in range(40):
+            bits = r.choice(n, size=int(r.choice(deg)), replace=False)
+            terms.append((float(r.integers(-5, 6)), int(sum(1 << int(b) for b in bits))))
+        poly = qs.spin_to_boolean(qs.SpinPolynomial(n, terms))
+    else:
+        w = r.integers(-9, 10, 60).astype(np.float64)
+        m = np.array([int(r.integers(0, 1 << n)) & int(r.integers(0, 1 << n)) for _ in range(60)], dtype=np.int64)
+        poly = qs.Polynomial(n, list(zip(w.tolist(), m.tolist())))
+    out = b200.empty(ctx.device, 1 << n, np.float64)
+    got = b200.build_cost_table(n, poly.weights, poly.masks, out) + (b200.table_symmetric(out, n),)
+    monkeypatch.setenv("QSB_NO_TABLE_STATS", "1")
+    out2 = b200.empty(ctx.device, 1 << n, np.float64)
+    want = b200.build_cost_table(n, poly.weights, poly.masks, out2) + (b200.table_symmetric(out2, n),)
+    t = np.asarray(out2)
+    assert want == (t.min(), t.max(), bool(np.array_equal(t, t[::-1])))
+    assert got == want
+    if kind in ("maxcut", "weighted_maxcut", "spin_even"):
+        assert got[2]
+
+
 def test_precompute_dyadic_matches_per_term_kernel(ctx, monkeypatch):
     poly = qs.maxcut_polynomial(qs.erdos_renyi(21, 0.5, seed=3))
     a = b200.empty(ctx.device, 1 << 21, np.float64)
