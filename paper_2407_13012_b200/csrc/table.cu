@@ -234,6 +234,77 @@ static int dyadic_shift(const double* w, uint64_t num_terms) {
   return -1;
 }
 
+// ---------------------------------------------------------------- float-weight path
+// Any weights: the reference's term-ordered sum, per x, from 0.0.  Tiles of 4096 x
+// sharing their high bits xh: the CTA compacts, in term order, the terms whose high mask
+// bits lie in xh (the others cannot match any x of the tile -- the reference skips them
+// too) into shared memory as (low mask, weight); each thread then runs that list over its
+// 16 x with a 32-bit mask test and a predicated add.  Same additions in the same order:
+// bit-exact for any weights.
+constexpr int kFChunk = 2048;  // compacted terms per pass
+
+__global__ void __launch_bounds__(kZThreads) k_precompute_tiled(const double* __restrict__ w,
+                                                                const uint64_t* __restrict__ m, uint64_t num_terms,
+                                                                double* __restrict__ out, uint64_t ntiles,
+                                                                IndexMap map) {
+  __shared__ double lw[kFChunk];
+  __shared__ uint32_t lm[kFChunk];
+  __shared__ uint32_t wcount[kZThreads / 32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t i0 = tile << kZT;
+    const uint64_t xh = map(i0);
+    double acc[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) acc[r] = 0.0;
+    const uint32_t xl = tid;  // this thread's x: xh | tid + 256 r
+    uint64_t k0 = 0;
+    while (k0 < num_terms) {
+      // ordered compaction of the next terms until the list is full or the terms end
+      uint32_t cnt = 0;
+      __syncthreads();  // the previous list has been consumed
+      while (k0 < num_terms && cnt + kZThreads <= (uint32_t)kFChunk) {
+        const uint64_t k = k0 + tid;
+        bool keep = false;
+        uint64_t mk = 0;
+        double wk = 0.0;
+        if (k < num_terms) {
+          mk = __ldg(&m[k]);
+          keep = ((mk & ~(uint64_t)(kZN - 1u)) & ~xh) == 0;
+          if (keep) wk = __ldg(&w[k]);
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) wcount[warp] = __popc(bal);
+        __syncthreads();
+        uint32_t before = cnt, total = cnt;
+#pragma unroll
+        for (int q = 0; q < kZThreads / 32; ++q) {
+          const uint32_t c = wcount[q];
+          if (q < (int)warp) before += c;
+          total += c;
+        }
+        if (keep) {
+          const uint32_t pos = before + __popc(bal & ((1u << lane) - 1u));
+          lm[pos] = (uint32_t)(mk & (kZN - 1u));
+          lw[pos] = wk;
+        }
+        cnt = total;
+        k0 += kZThreads;
+        __syncthreads();  // wcount reuse / the list is complete
+      }
+      for (uint32_t j = 0; j < cnt; ++j) {
+        const uint32_t mj = lm[j];
+        const double wj = lw[j];
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+          if (((xl | ((uint32_t)r << 8)) & mj) == mj) acc[r] = __dadd_rn(acc[r], wj);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) __stcs(out + i0 + tid + 256u * r, acc[r]);
+  }
+}
+
 // compact index: idx = T - vmin when T is an integer; flags non-integral values
 template <typename IDX>
 __global__ void k_compact(const double* __restrict__ t, uint64_t len, double vmin, IDX* __restrict__ idx,
@@ -322,6 +393,15 @@ static int precompute_into(qsb_ctx* ctx, const double* weights, const int64_t* m
     // d_small may still be read by queued kernels -> synchronous, stream-ordered copies
     QSB_CUDA(cudaMemcpyAsync(dw, weights, num_terms * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     QSB_CUDA(cudaMemcpyAsync(dm, masks, num_terms * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+  }
+  if (len >= kZN && (len & (kZN - 1)) == 0 && map.b >= (uint32_t)kZT && !(nz && atoi(nz) > 1)) {
+    // tiles of 4096 x with their terms compacted in order (QSB_NO_ZETA=2: the per-x kernel)
+    const uint64_t ntiles = len >> kZT;
+    const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * 4);
+    k_precompute_tiled<<<(unsigned)grid, kZThreads, 0, ctx->stream>>>(dw, dm, num_terms, out, ntiles, map);
+    QSB_CHECK_LAUNCH(ctx, "precompute (tiled)");
+    QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    return QSB_OK;
   }
   const uint64_t threads_needed = (len + kPreX - 1) / kPreX;
   const uint64_t blocks = (threads_needed + kPreThreads - 1) / kPreThreads;

@@ -179,6 +179,26 @@ def test_dyadic_table_stats_match_device_passes(ctx, kind, monkeypatch):
         assert got[2]
 
 
+@pytest.mark.parametrize("n,terms", [(12, 7), (16, 5000), (21, 700)])
+def test_precompute_float_tiled_bitwise(ctx, n, terms, monkeypatch):
+    """Float weights (no regrouping allowed): the tiled kernel (terms compacted per 4096-x
+    tile in order; > 2048 terms take several list passes) equals the oracle and the
+    per-x kernel (QSB_NO_ZETA=2) bit for bit."""
+    r = np.random.default_rng(300 + n)
+    w = r.normal(size=terms) * 2.5
+    m = np.array([int(x) & int(y) for x, y in zip(r.integers(0, 1 << n, terms), r.integers(0, 1 << n, terms))],
+                 dtype=np.int64)
+    m[::11] = 0
+    want = oracle.precompute_table(w, m, n)
+    out = b200.empty(ctx.device, 1 << n, np.float64)
+    b200.build_cost_table(n, w, m, out)
+    assert np.array_equal(np.asarray(out), want)
+    monkeypatch.setenv("QSB_NO_ZETA", "2")
+    out2 = b200.empty(ctx.device, 1 << n, np.float64)
+    b200.build_cost_table(n, w, m, out2)
+    assert np.array_equal(np.asarray(out2), want)
+
+
 def test_precompute_dyadic_matches_per_term_kernel(ctx, monkeypatch):
     poly = qs.maxcut_polynomial(qs.erdos_renyi(21, 0.5, seed=3))
     a = b200.empty(ctx.device, 1 << 21, np.float64)

@@ -1,5 +1,6 @@
-"""Cost-table build times: the exact int64 subset-sum path (dyadic weights) against the
-per-term kernel (QSB_NO_ZETA=1), and create_handle end to end.
+"""Cost-table build times: the default path (exact int64 subset-sum for dyadic weights,
+the tiled term-order kernel otherwise) against the tiled kernel (QSB_NO_ZETA=1) and the
+per-x kernel (QSB_NO_ZETA=2), and create_handle end to end.
 
     python tools/time_precompute.py [--max-n 32]
 
@@ -49,14 +50,18 @@ for name, n, mk in cases:
     t_fast = min(build(poly, out) for _ in range(2))
     a = np.asarray(out) if n <= 30 else None
     os.environ["QSB_NO_ZETA"] = "1"
+    t_tiled = min(build(poly, out) for _ in range(2))
+    same1 = bool(np.array_equal(a, np.asarray(out))) if a is not None else None
+    os.environ["QSB_NO_ZETA"] = "2"
     t_slow = min(build(poly, out) for _ in range(2))
     del os.environ["QSB_NO_ZETA"]
-    same = bool(np.array_equal(a, np.asarray(out))) if a is not None else "n/a (n>30: not copied)"
+    same = (same1 and bool(np.array_equal(a, np.asarray(out)))) if a is not None else "n/a (n>30: not copied)"
     out.free()
     t0 = time.perf_counter()
     h = qs.create_handle(poly, backend_name="b200")
     h.ctx.synchronize()
     t_create = 1e3 * (time.perf_counter() - t0)
     h.close()
-    print(f"{name:12s} n={n:2d} terms={poly.num_terms:5d}: table {t_fast:9.2f} ms (per-term kernel {t_slow:9.2f} ms, "
+    print(f"{name:12s} n={n:2d} terms={poly.num_terms:5d}: table {t_fast:9.2f} ms (tiled term-order kernel "
+          f"{t_tiled:9.2f} ms, per-x kernel {t_slow:9.2f} ms, "
           f"identical={same}); create_handle {t_create:9.2f} ms", flush=True)
