@@ -110,7 +110,7 @@ __device__ __forceinline__ void zeta_regs(long long (&v)[16]) {
       if (r & (1 << b)) v[r] += v[r ^ (1 << b)];
 }
 
-__global__ void __launch_bounds__(kZThreads) k_precompute_zeta(const long long* __restrict__ w,
+__global__ void __launch_bounds__(kZThreads, 4) k_precompute_zeta(const long long* __restrict__ w,
                                                                const uint64_t* __restrict__ m, uint64_t num_terms,
                                                                double* __restrict__ out, uint64_t ntiles, double scale,
                                                                IndexMap map, long long* __restrict__ minmax) {
@@ -368,7 +368,7 @@ static int precompute_into(qsb_ctx* ctx, const double* weights, const int64_t* m
       QSB_CUDA(cudaMemcpyAsync(dm, im.data(), nt * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
     }
     const uint64_t ntiles = len >> kZT;
-    const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * 3);  // 80 registers: 3 CTAs per SM
+    const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * 4);  // <= 64 registers: 4 CTAs per SM
     QSB_TRY(ensure_scratch(ctx, 64));
     long long* dmm = (long long*)ctx->d_scratch;
     k_minmax_init<<<1, 1, 0, ctx->stream>>>(dmm);
