@@ -649,9 +649,11 @@ def run_b200(args, rank: int, world: int, dist) -> None:
 
     # C3's 10^6 shots: draw from the simulated state (probability tree + per-shot
     # descent + cost gather on the device; indices/costs copied to the host).  One
-    # untimed warm-up draw allocates the context's sampler scratch (~0.1 s once).
+    # untimed warm-up draw of the same size allocates the context's sampler and shot
+    # scratch (once per context); the state is then re-simulated, so the timed draw
+    # starts from a fresh Z2-reduced state (tree over the lower half, no mirror copy).
+    qs.draw(h, args.shots, 0)
     qs.simulate(h, params)
-    qs.draw(h, 1000, 0)
     dev.sync()
     dev.timer_start()
     t0 = time.perf_counter()

@@ -237,6 +237,14 @@ int qsb_value_and_grad(qsb_ctx* ctx, qsb_table* t, double* ket, double* bra, int
 int qsb_sample(qsb_ctx* ctx, qsb_table* t, const double* amps, int n, uint64_t shots, uint64_t seed,
                int64_t* idx_out, double* cost_out, double* total_out);
 
+/* qsb_sample for a flip-symmetric state held as its lower half (the Z2 reduction:
+ * psi(x) = psi(~x), half_amps = psi(x) for x < 2^(n-1); same role as qsb_sample,
+ * backend.py:261-299).  The upper half of the reference's tree mirrors the lower half
+ * node for node, so only the lower half's levels are built; indices, costs and the
+ * root are bit-identical to qsb_sample on the materialised state. */
+int qsb_sample_sym(qsb_ctx* ctx, qsb_table* t, const double* half_amps, int n, uint64_t shots, uint64_t seed,
+                   int64_t* idx_out, double* cost_out, double* total_out);
+
 /* Sharded sampling (no reference counterpart: the reference samples one host array,
  * backend.py:261-299; SURVEY.md §8(e) "Sampling across GPUs").  A shard builds the
  * levels of its 2^n_local-amplitude subtree (kept in the context) and reports its

@@ -88,6 +88,7 @@ _SIGS = {
     "qsb_expectation": [_vp, _vp, _vp, C.c_uint, _dp],
     "qsb_value_and_grad": [_vp, _vp, _vp, _vp, _i32, _dp, _dp, C.c_uint, _i32, _dp, _dp, _dp],
     "qsb_sample": [_vp, _vp, _vp, _i32, _u64, _u64, _vp, _vp, _dp],
+    "qsb_sample_sym": [_vp, _vp, _vp, _i32, _u64, _u64, _vp, _vp, _dp],
     "qsb_sample_tree": [_vp, _vp, _i32, _dp],
     "qsb_shard_visit_run": [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _dp],
     "qsb_ipc_handle": [_vp, _vp, _vp],

@@ -125,9 +125,15 @@ struct CostView {
 
 // u_in == nullptr: u_s = U(seed, s) * root (the reference's draw); else u_s = u_in[s]
 // (a shard's residuals after the caller descended the levels above it).
+// half != 0 (a flip-symmetric state, Z2 reduction): amps and the stored levels hold
+// only the lower half x < N/2 of the full n-qubit tree.  Every node of the upper half
+// equals its mirror: full level-l node j == node N_l - 1 - j (pairwise sums of the
+// reversed leaves, and IEEE addition is commutative), so a lookup of node j reads the
+// lower-half node min(j, N_l - 1 - j) and a leaf x >= N/2 reads amplitude N - 1 - x.
+// L.n is the full tree's height; the root level is the caller's (h + h).
 __global__ void k_descend(const double2* __restrict__ amps, Levels L, const CostView table, uint64_t shots,
                           uint64_t seed, double root, const double* __restrict__ u_in, int64_t* __restrict__ idx_out,
-                          double* __restrict__ cost_out) {
+                          double* __restrict__ cost_out, int half) {
   for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < shots; s += (uint64_t)gridDim.x * blockDim.x) {
     double u;
     if (u_in) {
@@ -139,7 +145,12 @@ __global__ void k_descend(const double2* __restrict__ amps, Levels L, const Cost
     }
     uint64_t idx = 0;  // node at level l+1
     for (int l = L.n - 1; l >= L.k0; --l) {
-      const double left = L.base[L.off(l) + 2 * idx];
+      uint64_t j = 2 * idx;
+      if (half) {
+        const uint64_t nl = (L.N << 1) >> l;  // full-tree nodes at level l
+        if (j >= nl >> 1) j = nl - 1 - j;
+      }
+      const double left = L.base[L.off(l) + j];
       const bool right = u >= left;
       if (right) u = __dadd_rn(u, -left);
       idx = 2 * idx + (right ? 1 : 0);
@@ -151,7 +162,11 @@ __global__ void k_descend(const double2* __restrict__ amps, Levels L, const Cost
     const uint64_t leaf0 = idx << k0;
 #pragma unroll
     for (int e = 0; e < (1 << kK0); ++e)
-      if (e < (1 << k0)) t[e] = norm2_exact(amps[leaf0 + e]);
+      if (e < (1 << k0)) {
+        uint64_t x = leaf0 + e;
+        if (half && x >= L.N) x = 2 * L.N - 1 - x;
+        t[e] = norm2_exact(amps[x]);
+      }
     int lo[kK0 + 1];
     lo[0] = 0;
 #pragma unroll
@@ -204,7 +219,7 @@ int build_tree(qsb_ctx* ctx, const double2* a, int n, Levels* Lout, double* root
 // Descend `shots` shots on the tree in L (uniforms from the seed, or u_host); indices
 // and costs copied to the host arrays.
 int descend(qsb_ctx* ctx, qsb_table* t, const double2* a, const Levels& L, uint64_t shots, uint64_t seed, double root,
-            const double* u_host, int64_t* idx_out, double* cost_out) {
+            const double* u_host, int64_t* idx_out, double* cost_out, int half = 0) {
   QSB_TRY(ensure_shot_scratch(ctx, shots * (sizeof(int64_t) + sizeof(double) + (u_host ? sizeof(double) : 0))));
   int64_t* d_idx = (int64_t*)ctx->d_shots;
   double* d_cost = (double*)(d_idx + shots);
@@ -217,7 +232,8 @@ int descend(qsb_ctx* ctx, qsb_table* t, const double2* a, const Levels& L, uint6
   if (blocks > (uint64_t)ctx->num_sms * 64) blocks = (uint64_t)ctx->num_sms * 64;
   const CostView cv{t ? t->values : nullptr, t ? t->cidx : nullptr, t ? t->kind : 0, t ? t->vmin : 0.0};
   if (t && !t->values && !t->cidx) return invalid("sampling: the table has neither fp64 values nor a compact index");
-  k_descend<<<(unsigned)blocks, 256, 0, ctx->stream>>>(a, L, cv, shots, seed, root, d_u, d_idx, t ? d_cost : nullptr);
+  k_descend<<<(unsigned)blocks, 256, 0, ctx->stream>>>(a, L, cv, shots, seed, root, d_u, d_idx, t ? d_cost : nullptr,
+                                                       half);
   QSB_CHECK_LAUNCH(ctx, "sample descent");
   QSB_CUDA(cudaMemcpyAsync(idx_out, d_idx, shots * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
   if (t) QSB_CUDA(cudaMemcpyAsync(cost_out, d_cost, shots * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -246,6 +262,27 @@ int qsb_sample(qsb_ctx* ctx, qsb_table* t, const double* amps, int n, uint64_t s
   if (total_out) *total_out = root;
   if (!(fabs(root - 1.0) <= 1e-9)) return invalid("state is not normalized: sum of probabilities = %.17g", root);
   return descend(ctx, t, a, L, shots, seed, root, nullptr, idx_out, cost_out);
+}
+
+int qsb_sample_sym(qsb_ctx* ctx, qsb_table* t, const double* half_amps, int n, uint64_t shots, uint64_t seed,
+                   int64_t* idx_out, double* cost_out, double* total_out) {
+  if (ctx) QSB_CUDA(cudaSetDevice(ctx->device));  // launches go to the context's GPU
+  if (!ctx || !half_amps || !idx_out) return invalid("qsb_sample_sym: null argument");
+  if (shots < 1) return invalid("shots must be >= 1, got %llu", (unsigned long long)shots);
+  if (n < 2 || n > 62) return invalid("qsb_sample_sym: n=%d out of range", n);
+  if (t && n != t->n) return invalid("qsb_sample_sym: state has n=%d, table n=%d", n, t->n);
+  if (t && !cost_out) return invalid("qsb_sample_sym: table given without a cost output");
+  const double2* a = (const double2*)half_amps;
+  Levels L;
+  double h;
+  ctx->tree_n = -1;
+  QSB_TRY(build_tree(ctx, a, n - 1, &L, &h));  // levels 0..n-1 of the lower half
+  const double root = h + h;                   // full level n: lower root + its mirror
+  if (total_out) *total_out = root;
+  if (!(fabs(root - 1.0) <= 1e-9)) return invalid("state is not normalized: sum of probabilities = %.17g", root);
+  Levels F = L;
+  F.n = n;  // the full tree's height (node lookups fold into the stored half)
+  return descend(ctx, t, a, F, shots, seed, root, nullptr, idx_out, cost_out, 1);
 }
 
 int qsb_sample_tree(qsb_ctx* ctx, const double* amps, int n_local, double* root_out) {

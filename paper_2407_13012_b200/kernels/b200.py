@@ -239,14 +239,15 @@ def value_and_grad(ket: DeviceArray, bra: DeviceArray, table: DeviceArray, n: in
     return (val.value if want_value else None), dg, db
 
 
-def sample(amps: DeviceArray, table: DeviceArray | None, n: int, shots: int, seed: int):
-    """(indices int64[shots], costs f64[shots] or None)."""
+def sample(amps: DeviceArray, table: DeviceArray | None, n: int, shots: int, seed: int, half: bool = False):
+    """(indices int64[shots], costs f64[shots] or None).  half: amps holds only the lower
+    half of a flip-symmetric state (qsb_sample_sym; same draws as the full state)."""
     th = ensure_table_handle(table, n).ptr if table is not None else None
     idx = np.empty(shots, dtype=np.int64)
     cost = np.empty(shots, dtype=np.float64) if table is not None else None
     total = C.c_double()
     call(
-        "qsb_sample", _h(amps), th, amps.ptr, int(n), shots, int(seed) & ((1 << 64) - 1), idx.ctypes.data,
-        cost.ctypes.data if cost is not None else None, C.byref(total),
+        "qsb_sample_sym" if half else "qsb_sample", _h(amps), th, amps.ptr, int(n), shots,
+        int(seed) & ((1 << 64) - 1), idx.ctypes.data, cost.ctypes.data if cost is not None else None, C.byref(total),
     )
     return idx, cost

@@ -9,6 +9,8 @@ arrays directly.
 
 from __future__ import annotations
 
+import os
+
 from collections import Counter
 
 import numpy as np
@@ -50,7 +52,14 @@ def draw(handle: circuit.SimHandle, shots: int, seed: int) -> SampleSet:
     """Sample the handle's current state (no re-simulation)."""
     if shots < 1:
         raise ContractViolation(f"shots must be >= 1, got {shots}")
-    idx, costs = handle.ctx.kernels.sample(handle.state.data, handle.table.values.data, handle.n, int(shots), int(seed))
+    half = handle.state.half_view()
+    if half is not None and os.environ.get("QSB_NO_HALF_SAMPLE", "0") in ("", "0"):
+        # Z2-reduced state: draw from the lower half (no mirror copy; the same draws)
+        idx, costs = handle.ctx.kernels.sample(half, handle.table.values.data, handle.n, int(shots), int(seed),
+                                               half=True)
+    else:
+        idx, costs = handle.ctx.kernels.sample(handle.state.data, handle.table.values.data, handle.n, int(shots),
+                                               int(seed))
     handle.ctx._count(handle.n + 2)
     return SampleSet(shots=shots, seed=seed, indices=idx, costs=costs)
 

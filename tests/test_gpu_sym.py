@@ -53,6 +53,28 @@ def test_reduced_chain_vs_oracle_and_full(n, p, seed, monkeypatch):
     h.close()
 
 
+@pytest.mark.parametrize("n,p,seed", [(21, 2, 11), (24, 3, 12)])
+def test_half_state_sampling(n, p, seed, monkeypatch):
+    """Draws from the lower half of a Z2-reduced state (qsb_sample_sym: no mirror copy,
+    half the tree) are the draws of the materialised state, bit for bit."""
+    poly = random_instance(700 + seed, n)
+    params = random_params(seed, p)
+    table = oracle.precompute_table(poly.weights, poly.masks, n)
+    h = qs.create_handle(poly, backend_name="b200")
+    qs.simulate(h, params)
+    assert h.state.half_view() is not None  # the upper half is still unwritten
+    ss = qs.draw(h, 50000, seed)
+    assert h.state.half_view() is not None  # drawn from the half
+    assert (ss.indices >= (1 << (n - 1))).any() and (ss.indices < (1 << (n - 1))).any()
+    monkeypatch.setenv("QSB_NO_HALF_SAMPLE", "1")
+    full = qs.draw(h, 50000, seed)  # materialises the mirror, full tree
+    assert h.state.half_view() is None
+    assert np.array_equal(ss.indices, full.indices) and np.array_equal(ss.costs, full.costs)
+    idx, cost = oracle.sample(np.asarray(h.state.data), table, 50000, seed)
+    assert np.array_equal(ss.indices, idx) and np.array_equal(ss.costs, cost)
+    h.close()
+
+
 def test_reduced_batch_many():
     from paper_2407_13012_b200 import batch
 
