@@ -121,7 +121,11 @@ int ensure_shot_scratch(qsb_ctx* ctx, uint64_t bytes);
 // up to `want` device buffers of `bytes` each for forward checkpoints, as many as fit in
 // free HBM above a margin (QSB_CKPT_MARGIN_GB, default 8; QSB_NO_CKPT=1: none)
 int ensure_checkpoints(qsb_ctx* ctx, uint64_t bytes, int want, std::vector<double2*>& out);
-void release_checkpoints(qsb_ctx* ctx);
+void release_checkpoints(qsb_ctx* ctx, bool to_cache = false);
+// the large-block cache (ctx.cu): equal-size reuse of multi-GiB buffers
+void* big_take(int device, uint64_t bytes);
+bool big_put(int device, void* p, uint64_t bytes);
+void big_release(int device);
 // the walk that ensure_checkpoints handed buffers to has enqueued its last use of them
 void checkpoints_done(qsb_ctx* ctx);
 // build (cos, sin) of (sign * gamma * v) for v = vmin + k, k < nvals, with host libm

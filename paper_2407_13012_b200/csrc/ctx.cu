@@ -5,6 +5,8 @@
 
 #include <stdlib.h>
 
+#include <map>
+#include <unordered_map>
 #include <unordered_set>
 
 #include "common.cuh"
@@ -62,6 +64,11 @@ int ensure_sample_scratch(qsb_ctx* ctx, uint64_t bytes) {
   }
   ctx->tree_n = -1;
   cudaError_t e = cudaMalloc(&ctx->d_sample, bytes);
+  if (e == cudaErrorMemoryAllocation) {  // cached large blocks may be in the way
+    cudaGetLastError();
+    big_release(ctx->device);
+    e = cudaMalloc(&ctx->d_sample, bytes);
+  }
   if (e == cudaErrorMemoryAllocation) {
     cudaGetLastError();
     return ::qsb::cuda_fail(e, "sampler scratch");
@@ -98,6 +105,60 @@ int ensure_small(qsb_ctx* ctx, uint64_t bytes) {
   return QSB_OK;
 }
 
+// Large-block cache.  cudaMalloc / cudaFree of multi-GiB buffers cost milliseconds per
+// GiB (page-table work; cudaFree also synchronises the device), which made
+// create_handle / close and every first gradient of a fresh handle at n >= 26 cost
+// more than the E+grad itself.  Buffers above the stream-ordered pool's size (qsb_alloc
+// > 1 GiB) and forward checkpoints go back to a per-device cache on free (after their
+// stream has finished with them) and are handed out again for an equal size; an
+// allocation that runs out of memory, or a checkpoint set that needs memory the cache
+// holds, releases the cache first.  QSB_NO_BIGCACHE=1 disables it.
+namespace {
+constexpr uint64_t kBigKeep = 64ull << 30;
+std::mutex g_big_mu;
+std::multimap<uint64_t, void*> g_big[qsb::kMaxDevices];
+uint64_t g_big_bytes[qsb::kMaxDevices] = {};
+
+bool big_cache_enabled() {
+  const char* e = getenv("QSB_NO_BIGCACHE");
+  return !(e && atoi(e));
+}
+}  // namespace
+
+// a cached block of exactly `bytes`, or nullptr
+void* big_take(int device, uint64_t bytes) {
+  if (!big_cache_enabled()) return nullptr;
+  std::lock_guard<std::mutex> g(g_big_mu);
+  auto it = g_big[device].find(bytes);
+  if (it == g_big[device].end()) return nullptr;
+  void* p = it->second;
+  g_big[device].erase(it);
+  g_big_bytes[device] -= bytes;
+  return p;
+}
+
+// keep a block whose last uses have completed; false: the caller frees it
+bool big_put(int device, void* p, uint64_t bytes) {
+  if (!big_cache_enabled()) return false;
+  std::lock_guard<std::mutex> g(g_big_mu);
+  if (g_big_bytes[device] + bytes > kBigKeep) return false;
+  g_big[device].emplace(bytes, p);
+  g_big_bytes[device] += bytes;
+  return true;
+}
+
+void big_release(int device) {
+  std::multimap<uint64_t, void*> blocks;
+  {
+    std::lock_guard<std::mutex> g(g_big_mu);
+    blocks.swap(g_big[device]);
+    g_big_bytes[device] = 0;
+  }
+  if (blocks.empty()) return;
+  cudaSetDevice(device);
+  for (auto& kv : blocks) cudaFree(kv.second);
+}
+
 // Forward checkpoints.  Contexts holding them are registered so an allocation that runs
 // out of memory (on any thread) can take the memory back (release_all_checkpoints).
 // g_ck_mu guards every context's ck / ck_bytes / ck_busy; a context whose walk is being
@@ -106,20 +167,21 @@ namespace {
 std::mutex g_ck_mu;
 std::unordered_set<qsb_ctx*> g_ck_ctxs;
 
-void release_locked(qsb_ctx* ctx) {  // g_ck_mu held
+void release_locked(qsb_ctx* ctx, bool to_cache = false) {  // g_ck_mu held
   if (ctx->ck.empty()) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);  // kernels already enqueued may still read them
-  for (void* p : ctx->ck) cudaFree(p);
+  for (void* p : ctx->ck)
+    if (!to_cache || !qsb::big_put(ctx->device, p, ctx->ck_bytes)) cudaFree(p);
   ctx->ck.clear();
   ctx->ck_bytes = 0;
   g_ck_ctxs.erase(ctx);
 }
 }  // namespace
 
-void release_checkpoints(qsb_ctx* ctx) {
+void release_checkpoints(qsb_ctx* ctx, bool to_cache) {
   std::lock_guard<std::mutex> g(g_ck_mu);
-  release_locked(ctx);
+  release_locked(ctx, to_cache);
 }
 
 void release_all_checkpoints() {
@@ -135,7 +197,13 @@ int ensure_checkpoints(qsb_ctx* ctx, uint64_t bytes, int want, std::vector<doubl
   if ((off && atoi(off)) || want <= 0) return QSB_OK;
   std::lock_guard<std::mutex> g(g_ck_mu);
   if (ctx->ck_bytes != bytes) release_locked(ctx);
+  while ((int)ctx->ck.size() < want) {  // equal-size blocks from the large-block cache
+    void* p = big_take(ctx->device, bytes);
+    if (!p) break;
+    ctx->ck.push_back(p);
+  }
   if ((int)ctx->ck.size() < want) {
+    big_release(ctx->device);  // blocks of other sizes would only shrink the free memory
     const char* m = getenv("QSB_CKPT_MARGIN_GB");
     const uint64_t margin = (uint64_t)(m ? atof(m) : 8.0) << 30;
     size_t fr = 0, tot = 0;
@@ -149,9 +217,9 @@ int ensure_checkpoints(qsb_ctx* ctx, uint64_t bytes, int want, std::vector<doubl
       ctx->ck.push_back(p);
       fr -= bytes;
     }
-    ctx->ck_bytes = ctx->ck.empty() ? 0 : bytes;
-    if (!ctx->ck.empty()) g_ck_ctxs.insert(ctx);
   }
+  ctx->ck_bytes = ctx->ck.empty() ? 0 : bytes;
+  if (!ctx->ck.empty()) g_ck_ctxs.insert(ctx);
   for (int i = 0; i < want && i < (int)ctx->ck.size(); ++i) out.push_back((double2*)ctx->ck[i]);
   ctx->ck_busy = !out.empty();
   return QSB_OK;
@@ -275,7 +343,7 @@ int qsb_ctx_destroy(qsb_ctx* ctx) {
   if (!ctx) return QSB_OK;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-  release_checkpoints(ctx);
+  release_checkpoints(ctx, true);  // into the large-block cache (the next handle's walk)
   // the sampler's scratch is sized by the largest state drawn (0.5 GB at n=30): release it
   if (ctx->d_sample) cudaFree(ctx->d_sample);
   if (ctx->d_shots) cudaFree(ctx->d_shots);
@@ -398,11 +466,14 @@ bool pool_enabled() {
   return !(e && atoi(e));
 }
 
+std::unordered_map<void*, uint64_t> g_big_live;  // qsb_alloc blocks > kPooledMax (cacheable), guarded by g_alloc_mu
+
 int plain_alloc(qsb_ctx* ctx, uint64_t bytes, void** dptr) {
   cudaError_t e = cudaMalloc(dptr, bytes ? bytes : 16);
-  if (e == cudaErrorMemoryAllocation) {  // checkpoints / cached pool memory may be in the way
+  if (e == cudaErrorMemoryAllocation) {  // checkpoints / cached blocks / pool memory may be in the way
     cudaGetLastError();
     qsb::release_all_checkpoints();
+    qsb::big_release(ctx->device);
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) {
       cudaDeviceSynchronize();
@@ -444,6 +515,14 @@ int qsb_alloc(qsb_ctx* ctx, uint64_t bytes, void** dptr) {
       *dptr = nullptr;
     }
   }
+  if (bytes > kPooledMax) {
+    void* p = qsb::big_take(ctx->device, bytes);
+    if (!p) QSB_TRY(plain_alloc(ctx, bytes, &p));
+    std::lock_guard<std::mutex> g(g_alloc_mu);
+    g_big_live[p] = bytes;
+    *dptr = p;
+    return QSB_OK;
+  }
   return plain_alloc(ctx, bytes, dptr);
 }
 
@@ -459,13 +538,36 @@ int qsb_alloc_ipc(qsb_ctx* ctx, uint64_t bytes, void** dptr) {
 int qsb_free(qsb_ctx* ctx, void* dptr) {
   if (!dptr) return QSB_OK;
   bool pooled;
+  uint64_t big = 0;
   {
     std::lock_guard<std::mutex> g(g_alloc_mu);
     pooled = g_pooled.erase(dptr) > 0;
+    auto it = g_big_live.find(dptr);
+    if (it != g_big_live.end()) {
+      big = it->second;
+      g_big_live.erase(it);
+    }
   }
   if (ctx) QSB_CUDA(cudaSetDevice(ctx->device));
-  if (pooled && ctx) QSB_CUDA(cudaFreeAsync(dptr, ctx->stream));  // stream-ordered after its uses
-  else QSB_CUDA(cudaFree(dptr));
+  if (pooled && ctx) {
+    QSB_CUDA(cudaFreeAsync(dptr, ctx->stream));  // stream-ordered after its uses
+    return QSB_OK;
+  }
+  if (big) {  // the buffer's uses are done once its stream (or, with no context, the device) is
+    int dev = 0;
+    if (ctx) {
+      dev = ctx->device;
+      QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    } else {
+      cudaPointerAttributes at;
+      QSB_CUDA(cudaPointerGetAttributes(&at, dptr));
+      dev = at.device;
+      QSB_CUDA(cudaSetDevice(dev));
+      QSB_CUDA(cudaDeviceSynchronize());
+    }
+    if (qsb::big_put(dev, dptr, big)) return QSB_OK;
+  }
+  QSB_CUDA(cudaFree(dptr));
   return QSB_OK;
 }
 

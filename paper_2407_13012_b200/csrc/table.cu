@@ -453,6 +453,11 @@ static int finish_table(qsb_ctx* ctx, qsb_table* t, const TableStats* known = nu
     const size_t esz = kind == 1 ? 1 : 2;
     void* idx = nullptr;
     cudaError_t e = cudaMalloc(&idx, t->len * esz);
+    if (e == cudaErrorMemoryAllocation) {  // cached large blocks may be in the way
+      cudaGetLastError();
+      big_release(ctx->device);
+      e = cudaMalloc(&idx, t->len * esz);
+    }
     if (e != cudaSuccess) {  // compact table is an optimisation: fall back quietly
       cudaGetLastError();
       return QSB_OK;

@@ -9,7 +9,7 @@ from hypothesis import strategies as st
 
 import paper_2407_13012_b200 as qs
 
-from conftest import random_instance
+from conftest import random_instance, random_params
 
 pytestmark = pytest.mark.gpu
 
@@ -120,3 +120,23 @@ def test_batched_small_registers_equal_one_by_one():
         assert v == v1 and e == v1
         assert g.d_gammas == g1.d_gammas and g.d_betas == g1.d_betas
         h.close()
+
+
+def test_handles_reuse_large_blocks_bit_identically(monkeypatch):
+    """Multi-GiB buffers (state, table, bra, forward checkpoints) go to the large-block
+    cache on close and are reused by the next handle of the same size (ctx.cu): the
+    results are bit-identical to runs without the cache (QSB_NO_BIGCACHE=1)."""
+    params = random_params(5, 3)
+    polys = [qs.maxcut_polynomial(qs.random_regular(27, 4, seed=s)) for s in (1, 2, 1)]
+    got = []
+    for poly in polys:
+        h = qs.create_handle(poly, backend_name="b200")
+        v, g = qs.value_and_grad(h, params)
+        got.append((v, tuple(g.d_gammas), tuple(g.d_betas)))
+        h.close()
+    assert got[0] == got[2]
+    monkeypatch.setenv("QSB_NO_BIGCACHE", "1")
+    h = qs.create_handle(polys[1], backend_name="b200")
+    v, g = qs.value_and_grad(h, params)
+    h.close()
+    assert got[1] == (v, tuple(g.d_gammas), tuple(g.d_betas))
