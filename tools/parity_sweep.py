@@ -50,6 +50,10 @@ for k in range(count):
     e = qs.expectation(h, params)
     psi = np.asarray(qs.statevector(h, params))
     table = np.asarray(h.table.values.data)
+    qs.simulate(h, params)  # a Z2-reduced state (MaxCut) is drawn from its lower half
+    ss = qs.draw(h, 2000, k)
+    want_idx, want_cost = oracle.sample(np.asarray(h.state.data), table, 2000, k)
+    d_ok = bool(np.array_equal(ss.indices, want_idx) and np.array_equal(ss.costs, want_cost))
     h.close()
     want_t = oracle.precompute_table(poly.weights, poly.masks, n)
     want_psi = oracle.simulate(want_t, n, params.gammas, params.betas)
@@ -60,9 +64,9 @@ for k in range(count):
     e_err = max(abs(v - want_e), abs(e - want_e)) / max(1.0, abs(want_e))
     g_err = float(np.max(np.abs(got - want)) / max(np.max(np.abs(want)), 1e-300))
     s_err = float(np.max(np.abs(psi - want_psi)) / np.max(np.abs(want_psi)))
-    t_ok = bool(np.array_equal(table, want_t))
+    t_ok = bool(np.array_equal(table, want_t)) and d_ok
     worst = max(worst, e_err, g_err, s_err)
-    rows.append(f"{k:3d} {fam:8s} n={n:2d} p={p} terms={poly.num_terms:4d}  table bit-exact={t_ok}  "
+    rows.append(f"{k:3d} {fam:8s} n={n:2d} p={p} terms={poly.num_terms:4d}  table+draws bit-exact={t_ok}  "
                 f"E rel {e_err:.2e}  grad rel {g_err:.2e}  psi rel {s_err:.2e}")
     print(rows[-1], flush=True)
 with open(out_path, "w") as f:
