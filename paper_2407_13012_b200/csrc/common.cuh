@@ -126,6 +126,16 @@ void release_checkpoints(qsb_ctx* ctx, bool to_cache = false);
 void* big_take(int device, uint64_t bytes);
 bool big_put(int device, void* p, uint64_t bytes);
 void big_release(int device);
+// cudaMalloc that, when the device is full, gives the large-block cache back and retries
+inline cudaError_t dev_malloc(void** p, size_t bytes, int device) {
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    big_release(device);
+    e = cudaMalloc(p, bytes);
+  }
+  return e;
+}
 // the walk that ensure_checkpoints handed buffers to has enqueued its last use of them
 void checkpoints_done(qsb_ctx* ctx);
 // build (cos, sin) of (sign * gamma * v) for v = vmin + k, k < nvals, with host libm

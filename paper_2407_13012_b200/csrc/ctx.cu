@@ -49,7 +49,7 @@ int ensure_scratch(qsb_ctx* ctx, uint64_t bytes) {
     ctx->scratch_bytes = 0;
   }
   uint64_t want = bytes < (1u << 20) ? (1u << 20) : bytes;
-  QSB_CUDA(cudaMalloc(&ctx->d_scratch, want));
+  QSB_CUDA(dev_malloc((void**)&ctx->d_scratch, want, ctx->device));
   ctx->scratch_bytes = want;
   return QSB_OK;
 }
@@ -86,7 +86,7 @@ int ensure_shot_scratch(qsb_ctx* ctx, uint64_t bytes) {
     ctx->d_shots = nullptr;
     ctx->shots_bytes = 0;
   }
-  QSB_CUDA(cudaMalloc(&ctx->d_shots, bytes));
+  QSB_CUDA(dev_malloc((void**)&ctx->d_shots, bytes, ctx->device));
   ctx->shots_bytes = bytes;
   return QSB_OK;
 }
@@ -100,7 +100,7 @@ int ensure_small(qsb_ctx* ctx, uint64_t bytes) {
     ctx->small_bytes = 0;
   }
   uint64_t want = bytes < (1u << 16) ? (1u << 16) : bytes;
-  QSB_CUDA(cudaMalloc(&ctx->d_small, want));
+  QSB_CUDA(dev_malloc((void**)&ctx->d_small, want, ctx->device));
   ctx->small_bytes = want;
   return QSB_OK;
 }
@@ -114,7 +114,7 @@ int ensure_small(qsb_ctx* ctx, uint64_t bytes) {
 // allocation that runs out of memory, or a checkpoint set that needs memory the cache
 // holds, releases the cache first.  QSB_NO_BIGCACHE=1 disables it.
 namespace {
-constexpr uint64_t kBigKeep = 64ull << 30;
+constexpr uint64_t kBigKeep = 96ull << 30;
 std::mutex g_big_mu;
 std::multimap<uint64_t, void*> g_big[qsb::kMaxDevices];
 uint64_t g_big_bytes[qsb::kMaxDevices] = {};
@@ -157,6 +157,27 @@ void big_release(int device) {
   if (blocks.empty()) return;
   cudaSetDevice(device);
   for (auto& kv : blocks) cudaFree(kv.second);
+}
+
+// free cached blocks (largest first) until at least `need` bytes are free on the device
+// or the cache is empty -- cudaFree of multi-GiB blocks costs tens of ms each, so a size
+// change releases only what the new allocations need
+void big_release_until(int device, uint64_t need) {
+  cudaSetDevice(device);
+  for (;;) {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess || fr >= need) return;
+    void* p = nullptr;
+    {
+      std::lock_guard<std::mutex> g(g_big_mu);
+      if (g_big[device].empty()) return;
+      auto it = std::prev(g_big[device].end());
+      p = it->second;
+      g_big_bytes[device] -= it->first;
+      g_big[device].erase(it);
+    }
+    cudaFree(p);
+  }
 }
 
 // Forward checkpoints.  Contexts holding them are registered so an allocation that runs
@@ -203,9 +224,10 @@ int ensure_checkpoints(qsb_ctx* ctx, uint64_t bytes, int want, std::vector<doubl
     ctx->ck.push_back(p);
   }
   if ((int)ctx->ck.size() < want) {
-    big_release(ctx->device);  // blocks of other sizes would only shrink the free memory
     const char* m = getenv("QSB_CKPT_MARGIN_GB");
     const uint64_t margin = (uint64_t)(m ? atof(m) : 8.0) << 30;
+    // cached blocks of other sizes give back only what the missing checkpoints need
+    big_release_until(ctx->device, margin + bytes * (uint64_t)(want - (int)ctx->ck.size()) + bytes);
     size_t fr = 0, tot = 0;
     QSB_CUDA(cudaMemGetInfo(&fr, &tot));
     while ((int)ctx->ck.size() < want && fr > margin + bytes) {

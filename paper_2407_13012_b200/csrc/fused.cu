@@ -45,7 +45,7 @@ int prepare_luts(qsb_table* t, const std::vector<double>& ang_scales, const std:
     QSB_CUDA(cudaStreamSynchronize(ctx->stream));
     if (t->d_lut) cudaFree(t->d_lut);
     t->d_lut = nullptr;
-    QSB_CUDA(cudaMalloc(&t->d_lut, need * sizeof(double2)));
+    QSB_CUDA(dev_malloc((void**)&t->d_lut, need * sizeof(double2), ctx->device));
     t->h_lutbuf.assign(2 * need, 0.0);
   }
   double* h = t->h_lutbuf.data();
@@ -401,7 +401,7 @@ struct Runner {
     if (need > t->flut_cap) {  // grow, keeping this call's LUTs
       const uint64_t cap = std::max<uint64_t>(need, 2 * t->flut_cap);
       double2* nb = nullptr;
-      if (cudaMalloc(&nb, cap * sizeof(double2)) != cudaSuccess) {
+      if (dev_malloc((void**)&nb, cap * sizeof(double2), ctx->device) != cudaSuccess) {
         cudaGetLastError();
         return nullptr;
       }

@@ -481,7 +481,7 @@ static int finish_table(qsb_ctx* ctx, qsb_table* t, const TableStats* known = nu
     t->cidx = idx;
     t->kind = kind;
     t->nvals = (int)range + 1;
-    QSB_CUDA(cudaMalloc(&t->d_lut, (size_t)t->nvals * sizeof(double2)));
+    QSB_CUDA(dev_malloc((void**)&t->d_lut, (size_t)t->nvals * sizeof(double2), ctx->device));
     t->h_lutbuf.resize(2 * (size_t)t->nvals);
   }
   return QSB_OK;
