@@ -721,6 +721,11 @@ def run_b200(args, rank: int, world: int, dist) -> None:
                 "gbs": v[2] / (v[1] * 1e-3) / 1e9, "frac": v[2] / (v[1] * 1e-3) / 1e9 / peaks["hbm_gbs"]}
             for k, v in kinds.items()
         },
+        # per-kind fractions are on each kind's OWN algorithmic bytes: the Z2 reduction halves
+        # every kind's bytes and FP64 work, and forward checkpoints drop the ket store of the
+        # bra/ket kinds, so a compute-bound kind's fraction falls while its time falls too --
+        # compare ms_per_step across rounds (round 1: merged bra/ket A 43.4 ms per step)
+        "kernels_note": "frac = own algorithmic bytes / time / copy peak; compare ms_per_step across rounds",
         "sweeps_share_of_step": total_sweep_ms / ms,
         "step_hbm_gbs": all_bytes / (ms * 1e-3) / 1e9,
         # the whole step against the copy peak: on the bytes the step actually moves, and
