@@ -120,6 +120,11 @@ int qsb_ctx_launches(qsb_ctx* ctx, uint64_t* out);
 int qsb_alloc(qsb_ctx* ctx, uint64_t bytes, void** dptr);            /* np.empty, backend.py:133,165 */
 int qsb_alloc_ipc(qsb_ctx* ctx, uint64_t bytes, void** dptr);
 int qsb_free(qsb_ctx* ctx, void* dptr);                              /* eager release (StateBuffer.free) */
+/* Give back to the driver what the library keeps for reuse on `device`: the large-block
+ * cache of freed multi-GiB buffers, idle contexts' forward checkpoints and the
+ * stream-ordered pool's free memory (no reference counterpart: the reference's arrays
+ * are numpy's).  For callers that hand the GPU to another library. */
+int qsb_release_cached_memory(int device);
 /* CUDA IPC of device buffers for the sharded walk's fused qubit swap (dist.py):
  * export a 64-byte handle, open a peer process's buffer, close it; qsb_device_sync
  * waits for every kernel of this process (peer stores included) to complete. */

@@ -52,6 +52,7 @@ _SIGS = {
     "qsb_alloc": [_vp, _u64, C.POINTER(_vp)],
     "qsb_alloc_ipc": [_vp, _u64, C.POINTER(_vp)],
     "qsb_free": [_vp, _vp],
+    "qsb_release_cached_memory": [_i32],
     "qsb_h2d": [_vp, _vp, _vp, _u64],
     "qsb_d2h": [_vp, _vp, _vp, _u64],
     "qsb_d2d": [_vp, _vp, _vp, _u64],

@@ -593,6 +593,19 @@ int qsb_free(qsb_ctx* ctx, void* dptr) {
   return QSB_OK;
 }
 
+int qsb_release_cached_memory(int device) {
+  if (device < 0 || device >= qsb::kMaxDevices) return invalid("qsb_release_cached_memory: device %d", device);
+  QSB_CUDA(cudaSetDevice(device));
+  qsb::release_all_checkpoints();
+  qsb::big_release(device);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    QSB_CUDA(cudaDeviceSynchronize());
+    QSB_CUDA(cudaMemPoolTrimTo(pool, 0));
+  }
+  return QSB_OK;
+}
+
 // CUDA IPC for the sharded walk's fused qubit swap: a shard's spare buffers are exported
 // (64-byte handles, exchanged by the host over torch.distributed) and opened by every
 // peer process, whose swap-store kernels then write straight into them over NVLink.

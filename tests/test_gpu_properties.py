@@ -140,3 +140,11 @@ def test_handles_reuse_large_blocks_bit_identically(monkeypatch):
     v, g = qs.value_and_grad(h, params)
     h.close()
     assert got[1] == (v, tuple(g.d_gammas), tuple(g.d_betas))
+    monkeypatch.delenv("QSB_NO_BIGCACHE")
+    from paper_2407_13012_b200 import backend as be
+
+    be.release_cached_memory()  # everything cached goes back; later handles allocate afresh
+    h = qs.create_handle(polys[0], backend_name="b200")
+    v, g = qs.value_and_grad(h, params)
+    h.close()
+    assert got[0] == (v, tuple(g.d_gammas), tuple(g.d_betas))
