@@ -280,6 +280,10 @@ int qsb_nccl_version(int* version);
 int qsb_nccl_unique_id(void* id);
 int qsb_nccl_init(qsb_ctx* ctx, const void* id, int nranks, int rank, qsb_nccl** out);
 int qsb_nccl_all_to_all(qsb_nccl* c, const double* src, double* dst, uint64_t chunk_amps);
+/* Wait for the context stream's swaps, polling ncclCommGetAsyncError; on an NCCL error or
+ * after timeout_ms (< 0: none) the communicator is aborted (ncclCommAbort) and an error
+ * returned instead of a hang (failure detection). */
+int qsb_nccl_wait(qsb_nccl* c, int64_t timeout_ms);
 int qsb_nccl_destroy(qsb_nccl* c);
 /* amps[i] = re + i*im (a shard's part of |+> is 1/sqrt(2^n_global), fill_plus
  * numba_impl.py:40-44 for the whole register) */

@@ -109,6 +109,7 @@ _SIGS = {
     "qsb_nccl_unique_id": [_vp],
     "qsb_nccl_init": [_vp, _vp, _i32, _i32, C.POINTER(_vp)],
     "qsb_nccl_all_to_all": [_vp, _vp, _vp, _u64],
+    "qsb_nccl_wait": [_vp, C.c_int64],
     "qsb_nccl_destroy": [_vp],
 }
 _RESTYPES = {"qsb_last_error": C.c_char_p, "qsb_abi_version": _i32, "qsb_has_variants": _i32}

@@ -11,6 +11,9 @@
 // when there is one), so libqsb loads on machines without NCCL and the P2P transport
 // does not depend on it.  Only the types come from nccl.h.
 #include <dlfcn.h>
+
+#include <chrono>
+#include <thread>
 #include <nccl.h>
 
 #include "common.cuh"
@@ -37,6 +40,8 @@ struct NcclApi {
   ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*error_string)(ncclResult_t) = nullptr;
   ncclResult_t (*version)(int*) = nullptr;
+  ncclResult_t (*get_async_error)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*abort)(ncclComm_t) = nullptr;
 };
 
 const NcclApi& api() {
@@ -56,7 +61,8 @@ const NcclApi& api() {
     a.ok = sym(a.get_unique_id, "ncclGetUniqueId") && sym(a.comm_init_rank, "ncclCommInitRank") &&
            sym(a.comm_destroy, "ncclCommDestroy") && sym(a.group_start, "ncclGroupStart") &&
            sym(a.group_end, "ncclGroupEnd") && sym(a.send, "ncclSend") && sym(a.recv, "ncclRecv") &&
-           sym(a.error_string, "ncclGetErrorString") && sym(a.version, "ncclGetVersion");
+           sym(a.error_string, "ncclGetErrorString") && sym(a.version, "ncclGetVersion") &&
+           sym(a.get_async_error, "ncclCommGetAsyncError") && sym(a.abort, "ncclCommAbort");
     if (!a.ok) a.why = "libnccl.so.2 lacks a needed symbol";
   });
   return a;
@@ -141,6 +147,36 @@ int qsb_nccl_all_to_all(qsb_nccl* c, const double* src, double* dst, uint64_t ch
   }
   QSB_NCCL(a.group_end());
   return QSB_OK;
+}
+
+// Failure detection for the stream-ordered all-to-all: wait for the context stream while
+// polling the communicator's asynchronous error; on an NCCL error, or when the stream has
+// not finished after timeout_ms (a peer that died mid-swap leaves its partners' receives
+// pending forever), abort the communicator -- which releases the stuck kernels -- and
+// return an error instead of hanging.  timeout_ms < 0: no timeout.
+int qsb_nccl_wait(qsb_nccl* c, int64_t timeout_ms) {
+  if (!c) return invalid("qsb_nccl_wait: null argument");
+  if (!c->comm) return invalid("qsb_nccl_wait: the communicator was aborted");
+  QSB_CUDA(cudaSetDevice(c->ctx->device));
+  const NcclApi& a = api();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(c->ctx->stream);
+    if (q == cudaSuccess) return QSB_OK;
+    if (q != cudaErrorNotReady) QSB_CUDA(q);
+    ncclResult_t ar = ncclSuccess;
+    const ncclResult_t r = a.get_async_error(c->comm, &ar);
+    const bool failed = r != ncclSuccess || (ar != ncclSuccess && ar != ncclInProgress);
+    const int64_t ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+    if (failed || (timeout_ms >= 0 && ms > timeout_ms)) {
+      a.abort(c->comm);
+      c->comm = nullptr;
+      if (failed) return nccl_fail(r != ncclSuccess ? r : ar, "NCCL all-to-all (communicator aborted)");
+      set_error("NCCL all-to-all did not finish within %lld ms: communicator aborted", (long long)timeout_ms);
+      return QSB_ECUDA;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
 }
 
 int qsb_nccl_destroy(qsb_nccl* c) {

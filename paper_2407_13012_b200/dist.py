@@ -25,6 +25,7 @@ emulated in numpy by the tests (tests/test_dist_host.py).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -528,8 +529,11 @@ class TorchExchanger:
                  self.rank * chunk)
             self.commit(name, live, spare)
             return
-        if self._nccl:  # stream-ordered on the context stream: no host sync
+        if self._nccl:  # stream-ordered on the context stream
             call("qsb_nccl_all_to_all", self._nccl, v.ptr, s.ptr, chunk)
+            # failure detection: an NCCL error or a peer that never arrives aborts the
+            # communicator and raises here instead of hanging the next host sync
+            call("qsb_nccl_wait", self._nccl, int(os.environ.get("QSB_NCCL_TIMEOUT_MS", "600000")))
         elif self.cpu:  # gloo stand-in: D2H, all-to-all of host tensors, H2D into the spare
             host = torch.from_numpy(v.to_host().view(np.float64)).view(self.G, -1)
             recv = torch.empty_like(host)

@@ -214,6 +214,7 @@ def test_native_nccl_all_to_all_single_rank():
     call("qsb_nccl_init", dctx.handle, uid.ctypes.data, 1, 0, C.byref(comm))
     try:
         call("qsb_nccl_all_to_all", comm, src.ptr, dst.ptr, len(x))
+        call("qsb_nccl_wait", comm, 60000)  # completes: no async error, within the timeout
         assert np.array_equal(dst.to_host(), x)
     finally:
         call("qsb_nccl_destroy", comm)
