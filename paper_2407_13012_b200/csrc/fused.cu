@@ -1,6 +1,7 @@
 // Host orchestration of the fused hot path: sweep planning, simulate,
 // expectation, value_and_grad (adjoint walk over exactly two vectors) and the
 // Rx layer.  Reference: circuit.py:98-113, adjoint.py:37-77, backend.py:200-207.
+#include <nvtx3/nvToolsExt.h>
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
@@ -573,7 +574,19 @@ struct Runner {
     unsigned grid = 0;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->prof) QSB_TRY(prof_mark(ctx, &e0));
-    QSB_TRY(launch_sweep(ctx, nv, exact, a, &grid));
+    {
+      // NVTX range per sweep (kind names as in bench.py's "kernels"), so an ncu / nsys run
+      // can select sweeps by kind (ncu --nvtx --nvtx-include "braket_merged_A/"); a no-op
+      // unless a tool is attached
+      static const char* const kNames[12] = {"single_A", "single_B", "braket_A", "braket_B",
+                                             "single_merged_A", "single_merged_B", "braket_merged_A",
+                                             "braket_merged_B", "single_bridge_A", "single_bridge_B",
+                                             "braket_bridge_A", "braket_bridge_B"};
+      nvtxRangePushA(kNames[prof_kind(nv, mode, sh.is_a) % 12]);
+      const int rc = launch_sweep(ctx, nv, exact, a, &grid);
+      nvtxRangePop();
+      QSB_TRY(rc);
+    }
     if (ctx->prof) {
       QSB_TRY(prof_mark(ctx, &e1));
       ctx->prof_recs.push_back({e0, e1, prof_kind(nv, mode, sh.is_a), alg_bytes(nv, mode, flags)});
